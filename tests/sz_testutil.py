@@ -1,0 +1,52 @@
+"""Test helpers shared by the suites (golden fixtures, oracle params)."""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+GOLDEN_DIR = ROOT / "tests" / "golden"
+
+
+
+class Golden:
+    """Lazy view over tests/golden/{golden.npz,manifest.json}."""
+
+    def __init__(self):
+        self.manifest = json.loads((GOLDEN_DIR / "manifest.json").read_text())
+        self._npz = np.load(GOLDEN_DIR / "golden.npz")
+        self.cases = self.manifest["cases"]
+        self.corruptions = self.manifest["corruptions"]
+
+    def arr(self, cid: str, name: str) -> np.ndarray:
+        return self._npz[f"{cid}/{name}"]
+
+    def case(self, cid: str) -> dict:
+        return next(c for c in self.cases if c["id"] == cid)
+
+
+_GOLDEN = None
+
+
+def golden() -> Golden:
+    global _GOLDEN
+    if _GOLDEN is None:
+        _GOLDEN = Golden()
+    return _GOLDEN
+
+
+def golden_case_ids(tag: str | None = None):
+    return [c["id"] for c in golden().cases if tag is None or c["tag"] == tag]
+
+
+def oracle_params(case: dict):
+    from oracle import sz_oracle as O
+    return O.Params(case["fmt"], case["code_bits"], case["sentinel"], case["chunk"],
+                    case["abs32"])
