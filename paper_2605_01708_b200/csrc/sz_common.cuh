@@ -1,0 +1,265 @@
+// sz_common.cuh — device helpers shared by the SplitZip sm_100a kernels.
+//
+// Everything here is integer/bitwise work; nothing touches tensor cores.  The
+// kernels are HBM-bound streams, so the helpers are about moving bytes:
+// 256-bit global loads/stores (LDG.E.256 / STG.E.256 on sm_100a), a block-wide
+// exclusive scan in (item, thread) order, and a decoupled look-back over a
+// per-call tile-state array (flag and value packed into one 64-bit word so a
+// single relaxed store publishes both atomically).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/splitzip_b200.h"
+
+namespace sz {
+
+constexpr int kThreads = 256;          // CTA size of every streaming kernel
+constexpr int kWarps = kThreads / 32;
+
+// ---------------------------------------------------------------- formats
+// (word bytes, exponent bits, sign|mantissa bits) — formats.py:49-51.
+template <int FMT> struct Fmt;
+template <> struct Fmt<SZ_BF16> {
+  static constexpr int kWordBytes = 2, kExpBits = 8, kSmBits = 8;
+};
+template <> struct Fmt<SZ_E5M2> {
+  static constexpr int kWordBytes = 1, kExpBits = 5, kSmBits = 3;
+};
+template <> struct Fmt<SZ_E4M3> {
+  static constexpr int kWordBytes = 1, kExpBits = 4, kSmBits = 4;
+};
+// Elements per 32-byte vector ("slot").
+template <int FMT> constexpr int kEpv = 32 / Fmt<FMT>::kWordBytes;
+
+// ---------------------------------------------------------- memory access
+__device__ __forceinline__ void ld_stream256(const void* p, uint32_t (&r)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+        "=r"(r[6]), "=r"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void st256(void* p, const uint32_t (&r)[8]) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+               "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_stream128(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint2 ld_stream64(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+               : "=r"(v.x), "=r"(v.y)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Store `nbytes` (multiple of 2, <= 16) from packed words; the destination is
+// aligned to the largest power of two dividing nbytes.
+template <int NBYTES>
+__device__ __forceinline__ void st_packed(uint8_t* dst, const uint32_t* w) {
+  if constexpr (NBYTES == 16) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else if constexpr (NBYTES == 12) {
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    d[0] = w[0]; d[1] = w[1]; d[2] = w[2];
+  } else if constexpr (NBYTES == 8) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  } else if constexpr (NBYTES == 6) {
+    uint16_t* d = reinterpret_cast<uint16_t*>(dst);
+    d[0] = w[0] & 0xFFFF; d[1] = w[0] >> 16; d[2] = w[1] & 0xFFFF;
+  } else {
+    static_assert(NBYTES == 16, "unsupported store width");
+  }
+}
+// Byte-granular store clipped to [0, limit) — tail slots only.  Fully
+// unrolled so `w` stays in registers.
+template <int NBYTES>
+__device__ __forceinline__ void st_bytes_clipped(uint8_t* base, uint64_t off,
+                                                 const uint32_t* w, uint64_t limit) {
+#pragma unroll
+  for (int b = 0; b < NBYTES; ++b)
+    if (off + b < limit) base[off + b] = (w[b >> 2] >> (8 * (b & 3))) & 0xFF;
+}
+template <int NBYTES>
+__device__ __forceinline__ void ld_bytes_clipped(const uint8_t* base, uint64_t off, uint32_t* w,
+                                                 uint64_t limit) {
+#pragma unroll
+  for (int i = 0; i < (NBYTES + 3) / 4; ++i) w[i] = 0;
+#pragma unroll
+  for (int b = 0; b < NBYTES; ++b)
+    if (off + b < limit) w[b >> 2] |= static_cast<uint32_t>(base[off + b]) << (8 * (b & 3));
+}
+// Select word k of a small register array without dynamic indexing.
+template <int N>
+__device__ __forceinline__ uint32_t pick(const uint32_t* w, int k) {
+  uint32_t v = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) v = (i == k) ? w[i] : v;
+  return v;
+}
+
+// -------------------------------------------------------- bit shuffling
+// Four bytes, each < 16, to one 16-bit nibble group (element 0 low nibble) —
+// the nibble order of formats.py:180-183.
+__device__ __forceinline__ uint32_t pack_nib4(uint32_t b4) {
+  uint32_t t = b4 | (b4 >> 4);
+  return __byte_perm(t, 0, 0x4420);
+}
+// Four bytes, each < 8, to a 12-bit little-endian group (formats.py:184-189).
+__device__ __forceinline__ uint32_t pack_tri4(uint32_t b4) {
+  uint32_t u = (b4 | (b4 >> 5)) & 0x003F003Fu;
+  return (u | (u >> 10)) & 0xFFFu;
+}
+// Inverses.
+__device__ __forceinline__ uint32_t unpack_nib4(uint32_t x16) {
+  uint32_t t = __byte_perm(x16, 0, 0x4140);
+  return (t | (t << 4)) & 0x0F0F0F0Fu;
+}
+__device__ __forceinline__ uint32_t unpack_tri4(uint32_t x12) {
+  uint32_t u = (x12 | (x12 << 10)) & 0x003F003Fu;
+  return (u | (u << 5)) & 0x07070707u;
+}
+// Escape flags (bit 4 of each marked byte) of 4 elements -> 4-bit mask,
+// element 0 in bit 0.
+__device__ __forceinline__ uint32_t flags4(uint32_t marked4) {
+  uint32_t f = (marked4 >> 4) & 0x01010101u;
+  return (f * 0x01020408u) >> 24;
+}
+
+// Append G groups of W bits (W = 12 or 16) into a little-endian stream held
+// in `out` (ceil(G*W/32) words).
+template <int G, int W>
+__device__ __forceinline__ void concat_groups(const uint32_t (&grp)[G], uint32_t* out) {
+  constexpr int kWords = (G * W + 31) / 32;
+#pragma unroll
+  for (int i = 0; i < kWords; ++i) out[i] = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int bit = g * W;
+    const int wi = bit >> 5, sh = bit & 31;
+    out[wi] |= grp[g] << sh;
+    if (sh + W > 32) out[wi + 1] |= grp[g] >> (32 - sh);
+  }
+}
+// Extract group g of W bits from a little-endian stream.
+template <int W>
+__device__ __forceinline__ uint32_t group_bits(const uint32_t* in, int g) {
+  const int bit = g * W;
+  const int wi = bit >> 5, sh = bit & 31;
+  uint32_t v = in[wi] >> sh;
+  if (sh + W > 32) v |= in[wi + 1] << (32 - sh);
+  return v & ((1u << W) - 1);
+}
+
+// ------------------------------------------------------ block-wide scan
+// Exclusive scan of ITEMS x kThreads counts in (item, thread) order.
+// Returns the tile total; excl[i] receives this thread's prefix for item i.
+template <int ITEMS>
+struct BlockScanSmem {
+  uint32_t warp_tot[ITEMS * kWarps];
+  uint32_t total;
+};
+
+template <int ITEMS>
+__device__ __forceinline__ uint32_t block_scan(const uint32_t (&cnt)[ITEMS],
+                                               uint32_t (&excl)[ITEMS],
+                                               BlockScanSmem<ITEMS>& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    uint32_t v = cnt[i];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += o;
+    }
+    incl[i] = v;
+    if (lane == 31) sm.warp_tot[i * kWarps + warp] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int kN = ITEMS * kWarps;
+    static_assert(kN <= 32, "scan spine must fit one warp");
+    uint32_t v = lane < kN ? sm.warp_tot[lane] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += o;
+    }
+    if (lane < kN) sm.warp_tot[lane] = x - v;
+    if (lane == 31) sm.total = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) excl[i] = sm.warp_tot[i * kWarps + warp] + incl[i] - cnt[i];
+  return sm.total;
+}
+
+// ------------------------------------------------ decoupled look-back
+// Tile state word: bits 62-63 flag (0 empty, 1 aggregate, 2 inclusive
+// prefix), bits 0-61 value.  The array must be zeroed before the launch.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPrefix = 2ull << 62;
+constexpr uint64_t kValueMask = (1ull << 62) - 1;
+
+// Called by ALL lanes of one warp.  Publishes `agg` for `tile`, walks back to
+// the nearest inclusive prefix, publishes this tile's inclusive prefix and
+// returns the exclusive prefix (in every lane).
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* states, uint64_t tile,
+                                                  uint64_t agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(&states[0], kFlagPrefix | agg);
+    return 0;
+  }
+  if (lane == 0) st_relaxed(&states[tile], kFlagAgg | agg);
+  uint64_t excl = 0;
+  int64_t pred = static_cast<int64_t>(tile) - 1;
+  while (true) {
+    const int64_t idx = pred - lane;
+    uint64_t s = idx >= 0 ? ld_relaxed(&states[idx]) : kFlagPrefix;
+    uint32_t flag = static_cast<uint32_t>(s >> 62);
+    if (__any_sync(0xffffffffu, flag == 0)) {
+      __nanosleep(32);
+      continue;
+    }
+    const uint32_t pmask = __ballot_sync(0xffffffffu, flag == 2);
+    uint64_t v = s & kValueMask;
+    int stop = pmask ? __ffs(pmask) - 1 : 31;
+    if (lane > stop) v = 0;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    excl += v;
+    if (pmask) break;
+    pred -= 32;
+  }
+  if (lane == 0) st_relaxed(&states[tile], kFlagPrefix | (excl + agg));
+  return excl;
+}
+
+// Atomic "keep the smallest index" into a zero-initialised slot, storing ~idx.
+__device__ __forceinline__ void record_first(uint64_t* slot, uint64_t idx) {
+  atomicMax(reinterpret_cast<unsigned long long*>(slot),
+            static_cast<unsigned long long>(~idx));
+}
+
+}  // namespace sz

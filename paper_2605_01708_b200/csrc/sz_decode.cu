@@ -1,0 +1,611 @@
+// sz_decode.cu — K3 (chunk offsets) + K4 (decode) for sm_100a.
+//
+// Replaces codec.py:421-536 (decode, _decode_dense, _escape_indices).
+//
+// K3: exclusive scan of the u32 per-chunk escape counts into u64 ordinal
+//     offsets (the `starts = repeat(chunk*c, counts)` of codec.py:520-523 in
+//     prefix form), single pass with decoupled look-back; also checks
+//     sum(counts) == M (codec.py:513-514).
+// K4: one CTA per tile of ITEMS x 256 x EPV elements:
+//   - vector loads of the tile's nibble/3-bit code plane and its
+//     sign|mantissa plane;
+//   - the tile's escapes (explicit modes) are scattered into a shared-memory
+//     bitmap + value array, with every per-escape check of _escape_indices
+//     done on the way (position < chunk, index < N, strictly increasing);
+//   - per 2 codes one shared-memory "pair LUT" load gives both exponents plus
+//     range / sentinel flags; escaped elements take their raw exponent from
+//     shared memory (the reference's sparse overwrite, codec.py:477, done in
+//     registers so every output byte is written exactly once);
+//   - words are rebuilt with byte permutes and written with 256-bit stores.
+//   Sentinel mode finds each marked element's escape ordinal with a block scan
+//   + decoupled look-back over per-tile mark counts (codec.py:459-467).
+// Corruption never faults: every index is bounds-checked, and each failed
+// check records its smallest offending ordinal/element in sz_decode_status;
+// the host raises CorruptionError in the reference's check order.
+#include "sz_common.cuh"
+
+namespace sz {
+
+// ------------------------------------------------------------------ K3
+struct OffsetsArgs {
+  const uint64_t* m_ptr;
+  const uint32_t* counts;
+  uint64_t n_counts;
+  uint64_t m;
+  uint64_t* offsets;      // n_counts + 1 entries
+  uint64_t* states;
+  unsigned long long* tile_counter;
+  uint64_t num_tiles;
+  sz_decode_status* status;
+};
+
+constexpr int kOffItems = 16;  // counts per thread
+
+__global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) {
+  __shared__ uint64_t warp_tot[kWarps];
+  __shared__ unsigned long long s_tile;
+  __shared__ uint64_t s_excl, s_total;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(a.tile_counter, 1ull);
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t base = (tile * kThreads + tid) * kOffItems;
+  uint32_t v[kOffItems];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int j = 0; j < kOffItems; ++j) {
+    v[j] = base + j < a.n_counts ? a.counts[base + j] : 0u;
+    sum += v[j];
+  }
+  // block exclusive scan of per-thread sums (u64: corrupted counts may be huge)
+  uint64_t incl = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = lane < kWarps ? warp_tot[lane] : 0, xw = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t o = __shfl_up_sync(0xffffffffu, xw, d);
+      if (lane >= d) xw += o;
+    }
+    if (lane < kWarps) warp_tot[lane] = xw - w;
+    const uint64_t total = __shfl_sync(0xffffffffu, xw, 31);
+    const uint64_t ex = lookback_warp(a.states, tile, total);
+    if (lane == 0) {
+      s_excl = ex;
+      s_total = ex + total;
+    }
+  }
+  __syncthreads();
+  uint64_t run = s_excl + warp_tot[warp] + incl - sum;
+#pragma unroll
+  for (int j = 0; j < kOffItems; ++j) {
+    if (base + j < a.n_counts) a.offsets[base + j] = run;
+    run += v[j];
+  }
+  if (tile == a.num_tiles - 1 && tid == 0) {
+    a.offsets[a.n_counts] = s_total;
+    a.status->counts_total = s_total;
+    const uint64_t m = a.m_ptr ? *a.m_ptr : a.m;
+    if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_COUNTS_TOTAL);
+  }
+}
+
+// ------------------------------------------------------------------ K4
+struct DecodeArgs {
+  const uint64_t* m_ptr;     // optional device-resident M
+  const uint8_t* codes;
+  const uint8_t* sm;
+  const uint64_t* offsets;   // chunked mode
+  const void* positions;
+  const uint8_t* values;
+  uint64_t n, m;
+  uint8_t* out;
+  sz_decode_status* status;
+  uint64_t* states;          // sentinel look-back
+  unsigned long long* tile_counter;
+  uint64_t num_tiles;
+  uint64_t n_chunks;
+  uint64_t codes_len, sm_len;
+  uint32_t chunk;
+  int32_t chunk_shift;
+};
+
+template <int NBYTES>
+__device__ __forceinline__ void ld_packed(const uint8_t* src, uint32_t* w) {
+  if constexpr (NBYTES == 16) {
+    const uint4 v = ld_stream128(src);
+    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+  } else if constexpr (NBYTES == 12) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    w[0] = __ldg(s); w[1] = __ldg(s + 1); w[2] = __ldg(s + 2);
+  } else if constexpr (NBYTES == 8) {
+    const uint2 v = ld_stream64(src);
+    w[0] = v.x; w[1] = v.y;
+  } else if constexpr (NBYTES == 6) {
+    const uint16_t* s = reinterpret_cast<const uint16_t*>(src);
+    w[0] = __ldg(s) | (static_cast<uint32_t>(__ldg(s + 1)) << 16);
+    w[1] = __ldg(s + 2);
+  }
+}
+
+template <int POSB>
+__device__ __forceinline__ uint64_t load_pos(const void* p, uint64_t o) {
+  if constexpr (POSB == 1) return static_cast<const uint8_t*>(p)[o];
+  else if constexpr (POSB == 2) return static_cast<const uint16_t*>(p)[o];
+  else return static_cast<const uint32_t*>(p)[o];
+}
+
+template <int FMT>
+__device__ __forceinline__ void rebuild_group(uint32_t e4, uint32_t a4, uint32_t* outw, int g) {
+  if constexpr (FMT == SZ_BF16) {
+    const uint32_t lo4 = (a4 & 0x7F7F7F7Fu) | ((e4 << 7) & 0x80808080u);
+    const uint32_t hi4 = (a4 & 0x80808080u) | ((e4 >> 1) & 0x7F7F7F7Fu);
+    outw[2 * g] = __byte_perm(lo4, hi4, 0x5140);
+    outw[2 * g + 1] = __byte_perm(lo4, hi4, 0x7362);
+  } else if constexpr (FMT == SZ_E5M2) {
+    outw[g] = ((a4 << 5) & 0x80808080u) | (e4 << 2) | (a4 & 0x03030303u);
+  } else {
+    outw[g] = ((a4 << 4) & 0x80808080u) | (e4 << 3) | (a4 & 0x07070707u);
+  }
+}
+
+// Warp-cooperative lower_bound over sorted u32 positions [0, m) (abs32 mode).
+__device__ uint64_t warp_lower_bound(const uint32_t* pos, uint64_t m, uint64_t target) {
+  const int lane = threadIdx.x & 31;
+  uint64_t lo = 0, hi = m;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const uint64_t step = (hi - lo) / 33 + 1;
+    const uint64_t probe = lo + (lane + 1) * step;
+    const bool less = probe < hi && pos[probe - 1] < target;  // all < probe are < target
+    const uint32_t bal = __ballot_sync(0xffffffffu, less);
+    const int cnt = __popc(bal);  // lanes 0..cnt-1 say "less" (monotone if sorted)
+    const uint64_t nlo = lo + cnt * step;
+    const uint64_t nhi = min(hi, lo + (cnt + 1) * step);
+    lo = nlo;
+    hi = max(nhi, nlo);
+  }
+  const uint64_t probe = lo + lane;
+  const bool less = probe < hi && pos[probe] < target;
+  return lo + __popc(__ballot_sync(0xffffffffu, less));
+}
+
+template <int FMT, int CB, int POSB, int ITEMS>
+__global__ void __launch_bounds__(kThreads)
+    decode_kernel(const __grid_constant__ sz_params p, const DecodeArgs a) {
+  constexpr int EPV = kEpv<FMT>;
+  constexpr int G = EPV / 4;
+  constexpr int WB = Fmt<FMT>::kWordBytes;
+  constexpr int SMB = Fmt<FMT>::kSmBits;
+  constexpr int CBYTES = EPV * CB / 8;
+  constexpr int SBYTES = EPV * SMB / 8;
+  constexpr int CWORDS = (CBYTES + 3) / 4;
+  constexpr int SWORDS = (SBYTES + 3) / 4;
+  constexpr int SLOTS = ITEMS * kThreads;
+  constexpr uint64_t TILE = static_cast<uint64_t>(SLOTS) * EPV;
+  constexpr bool SENT = POSB == 0;
+  constexpr bool ABS = POSB == 4;
+  constexpr int LUT2 = CB == 4 ? 256 : 64;
+  constexpr int kOffStage = 1024;
+
+  // pair LUT: byte0/1 = exponents of the two codes, byte2 bit0/1 = code out of
+  // range (not counting sentinel marks), byte3 bit0/1 = sentinel mark.
+  __shared__ uint32_t lut2[LUT2];
+  __shared__ uint32_t bitmap[SENT ? 1 : TILE / 32];
+  __shared__ uint8_t vals[SENT ? 4 : TILE];
+  __shared__ uint64_t s_off[SENT || ABS ? 1 : kOffStage + 1];
+  __shared__ BlockScanSmem<ITEMS> scan_sm;
+  __shared__ unsigned long long s_tile;
+  __shared__ uint64_t s_lo, s_hi, s_ka, s_excl;
+
+  const int tid = threadIdx.x;
+  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
+  constexpr uint32_t kCodeMask = (1u << CB) - 1;
+  const uint32_t sentinel_code = SENT ? kCodeMask : 0xFFu;
+  for (int i = tid; i < LUT2; i += kThreads) {
+    const uint32_t c0 = i & kCodeMask, c1 = (i >> CB) & kCodeMask;
+    const uint32_t mk0 = c0 == sentinel_code, mk1 = c1 == sentinel_code;
+    const uint32_t bad0 = !mk0 && c0 >= p.n_entries, bad1 = !mk1 && c1 >= p.n_entries;
+    lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | ((bad0 | (bad1 << 1)) << 16) |
+              ((mk0 | (mk1 << 1)) << 24);
+  }
+  if (tid == 0) s_tile = SENT ? atomicAdd(a.tile_counter, 1ull) : blockIdx.x;
+  if constexpr (!SENT) {
+    for (int i = tid; i < static_cast<int>(TILE / 32); i += kThreads) bitmap[i] = 0;
+  }
+  __syncthreads();
+  const uint64_t tile = s_tile;
+  const uint64_t s = tile * TILE;
+  const uint64_t e = min(s + TILE, n);
+
+  // ---- loads of both planes for all items
+  uint32_t cw[ITEMS][CWORDS], sw[ITEMS][SWORDS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t e0 = s + static_cast<uint64_t>(i * kThreads + tid) * EPV;
+    const uint64_t coff = e0 * CB / 8, soff = e0 * SMB / 8;
+    if (e0 + EPV <= n) {
+      ld_packed<CBYTES>(a.codes + coff, cw[i]);
+      ld_packed<SBYTES>(a.sm + soff, sw[i]);
+    } else {
+      ld_bytes_clipped<CBYTES>(a.codes, coff, cw[i], e0 < n ? a.codes_len : 0);
+      ld_bytes_clipped<SBYTES>(a.sm, soff, sw[i], e0 < n ? a.sm_len : 0);
+    }
+  }
+
+  // ---- distributed per-ordinal checks (independent of the chunk counts)
+  {
+    const uint64_t q = (m + a.num_tiles - 1) / a.num_tiles;
+    const uint64_t o0 = tile * q, o1 = min(o0 + q, m);
+    const uint32_t exp_bins = 1u << Fmt<FMT>::kExpBits;
+    for (uint64_t o = o0 + tid; o < o1; o += kThreads) {
+      const uint32_t v = a.values[o];
+      if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+      else if (!(p.enc_lut[v] & 0x10)) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+      if constexpr (ABS) {
+        const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
+        const uint32_t pv = pos[o];
+        if (pv >= n) record_first(&a.status->first_inv[SZ_DEC_ABS_PAST_END], o);
+        if (o > 0 && pv <= pos[o - 1]) record_first(&a.status->first_inv[SZ_DEC_ABS_NOT_INC], o);
+      }
+    }
+  }
+
+  // ---- pad-bit checks on the final bytes (codec.py:441-442, 236-237)
+  if (tile == a.num_tiles - 1 && tid == 0) {
+    const uint32_t cbits = static_cast<uint32_t>((n * CB) & 7);
+    if (cbits && (a.codes[a.codes_len - 1] >> cbits)) record_first(&a.status->first_inv[SZ_DEC_CODE_PAD], 0);
+    if constexpr (SMB != 8) {
+      const uint32_t sbits = static_cast<uint32_t>((n * SMB) & 7);
+      if (sbits && (a.sm[a.sm_len - 1] >> sbits)) record_first(&a.status->first_inv[SZ_DEC_SM_PAD], 0);
+    }
+  }
+
+  // ---- stage this tile's escapes (explicit modes)
+  if constexpr (!SENT) {
+    if constexpr (ABS) {
+      if (tid < 32) {
+        const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
+        const uint64_t lo = warp_lower_bound(pos, m, s);
+        const uint64_t hi = warp_lower_bound(pos, m, e);
+        if (tid == 0) { s_lo = lo; s_hi = max(hi, lo); }
+      }
+      __syncthreads();
+      const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
+      for (uint64_t o = s_lo + tid; o < s_hi; o += kThreads) {
+        const uint64_t idx = pos[o];
+        if (idx >= s && idx < e) {
+          const uint32_t rel = static_cast<uint32_t>(idx - s);
+          atomicOr(&bitmap[rel >> 5], 1u << (rel & 31));
+          vals[rel] = a.values[o];
+        }
+      }
+    } else {
+      const uint64_t ka = s / a.chunk, kb = (e - 1) / a.chunk;
+      const uint64_t nk = kb - ka + 2;   // offsets ka..kb+1
+      const bool staged = nk <= kOffStage + 1;
+      if (staged)
+        for (uint64_t i = tid; i < nk; i += kThreads) s_off[i] = a.offsets[ka + i];
+      if (tid == 0) {
+        s_ka = ka;
+        s_lo = min(a.offsets[ka], m);
+        s_hi = min(a.offsets[kb + 1], m);
+      }
+      __syncthreads();
+      const uint64_t* off = staged ? s_off : a.offsets + ka;
+      for (uint64_t o = s_lo + tid; o < s_hi; o += kThreads) {
+        // chunk of ordinal o: last k in [0, nk-1) with off[k] <= o
+        uint64_t lo = 0, hi = nk - 1;
+        while (hi - lo > 1) {
+          const uint64_t mid = (lo + hi) >> 1;
+          if (off[mid] <= o) lo = mid; else hi = mid;
+        }
+        const uint64_t k = ka + lo;
+        const uint64_t pv = load_pos<POSB>(a.positions, o);
+        if (pv >= a.chunk) {
+          record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+          continue;
+        }
+        const uint64_t idx = k * a.chunk + pv;
+        if (idx >= n) {
+          record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+          continue;
+        }
+        if (o > off[lo] && load_pos<POSB>(a.positions, o - 1) >= pv)
+          record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+        if (idx >= s && idx < e) {
+          const uint32_t rel = static_cast<uint32_t>(idx - s);
+          atomicOr(&bitmap[rel >> 5], 1u << (rel & 31));
+          vals[rel] = a.values[o];
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- dense decode: pair-LUT exponents, flags
+  uint32_t eg[ITEMS][G], ag[ITEMS][G];
+  uint32_t marks[ITEMS];
+  uint32_t cnt[ITEMS];
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t e0 = s + static_cast<uint64_t>(i * kThreads + tid) * EPV;
+    const int nv = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
+    uint32_t bad = 0, mk = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      uint32_t l0, l1;
+      if constexpr (CB == 4) {
+        const uint32_t cb16 = group_bits<16>(cw[i], g);
+        l0 = lut2[cb16 & 0xFF];
+        l1 = lut2[cb16 >> 8];
+      } else {
+        const uint32_t cb12 = group_bits<12>(cw[i], g);
+        l0 = lut2[cb12 & 0x3F];
+        l1 = lut2[cb12 >> 6];
+      }
+      eg[i][g] = __byte_perm(l0, l1, 0x5410);
+      const uint32_t v = min(max(nv - 4 * g, 0), 4);
+      const uint32_t vmask = (1u << v) - 1u;
+      bad |= ((((l0 >> 16) & 3) | (((l1 >> 16) & 3) << 2)) & vmask) << (4 * g);
+      if constexpr (SENT) mk |= ((((l0 >> 24) & 3) | (((l1 >> 24) & 3) << 2)) & vmask) << (4 * g);
+      if constexpr (SMB == 8) ag[i][g] = sw[i][g];
+      else if constexpr (SMB == 4) ag[i][g] = unpack_nib4(group_bits<16>(sw[i], g));
+      else ag[i][g] = unpack_tri4(group_bits<12>(sw[i], g));
+    }
+    if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
+    marks[i] = mk;
+    cnt[i] = __popc(mk);
+  }
+
+  if constexpr (SENT) {
+    // ordinal of each marked element: block scan + look-back over mark counts
+    uint32_t excl[ITEMS];
+    const uint32_t total = block_scan<ITEMS>(cnt, excl, scan_sm);
+    if (tid < 32) {
+      const uint64_t ex = lookback_warp(a.states, tile, total);
+      if (tid == 0) {
+        s_excl = ex;
+        if (tile == a.num_tiles - 1) {
+          a.status->marks_total = ex + total;
+          if (ex + total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_SENTINEL_COUNT);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t mk = marks[i];
+      if (!mk) continue;
+      uint64_t ord = s_excl + excl[i];
+      // fully unrolled over (group, byte) so eg stays in registers
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if ((mk >> (4 * g + b)) & 1u) {
+            const uint32_t v = ord < m ? a.values[ord] : 0u;
+            ++ord;
+            eg[i][g] = (eg[i][g] & ~(0xFFu << (8 * b))) | (v << (8 * b));
+          }
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const uint32_t slot = i * kThreads + tid;
+      uint32_t bm;
+      if constexpr (EPV == 32) bm = bitmap[slot];
+      else bm = (bitmap[slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
+      if (!bm) continue;
+      const uint64_t e0 = s + static_cast<uint64_t>(slot) * EPV;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          constexpr int kDummy = 0;
+          const int j = 4 * g + b;
+          if ((bm >> j) & 1u) {
+            uint32_t code;
+            if constexpr (CB == 4) code = (cw[i][j >> 3] >> (4 * (j & 7))) & 0xF;
+            else code = (group_bits<12>(cw[i], g) >> (3 * b)) & 7;
+            if (code != kDummy) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+            const uint32_t v = vals[slot * EPV + j];
+            eg[i][g] = (eg[i][g] & ~(0xFFu << (8 * b))) | (v << (8 * b));
+          }
+        }
+      }
+    }
+  }
+
+  // ---- rebuild words and store
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint64_t e0 = s + static_cast<uint64_t>(i * kThreads + tid) * EPV;
+    uint32_t ow[8];
+#pragma unroll
+    for (int g = 0; g < G; ++g) rebuild_group<FMT>(eg[i][g], ag[i][g], ow, g);
+    if (e0 + EPV <= n) {
+      st256(a.out + e0 * WB, ow);
+    } else if (e0 < n) {
+      st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
+    }
+  }
+}
+
+__global__ void check_values_kernel(const uint8_t* __restrict__ values, uint64_t m,
+                                    const __grid_constant__ sz_params p, sz_decode_status* st) {
+  const uint32_t exp_bins = 1u << (p.fmt == SZ_BF16 ? 8 : (p.fmt == SZ_E5M2 ? 5 : 4));
+  for (uint64_t o = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; o < m;
+       o += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t v = values[o];
+    if (v >= exp_bins) record_first(&st->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+    else if (!(p.enc_lut[v] & 0x10)) record_first(&st->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+  }
+}
+
+}  // namespace sz
+
+// ============================================================ host dispatch
+namespace {
+using namespace sz;
+
+constexpr int kDecodeItems = 2;
+
+uint64_t decode_tile_for(uint32_t fmt) {
+  return static_cast<uint64_t>(kDecodeItems) * kThreads * (fmt == SZ_BF16 ? 16 : 32);
+}
+uint64_t offsets_tiles(uint64_t n_counts) {
+  const uint64_t per = static_cast<uint64_t>(kThreads) * kOffItems;
+  return (n_counts + per - 1) / per;
+}
+
+struct DecodeWs {
+  uint64_t* offsets;
+  uint64_t* off_states;
+  unsigned long long* off_counter;
+  uint64_t* dec_states;
+  unsigned long long* dec_counter;
+  size_t zero_bytes;  // prefix of the workspace that must be zeroed
+  size_t total;
+};
+
+DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
+  DecodeWs w{};
+  const bool chunked = !p->sentinel && !p->abs32;
+  const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size : 0;
+  const uint64_t otiles = chunked ? offsets_tiles(nchunks) : 0;
+  const uint64_t dtiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
+  uint64_t* b = static_cast<uint64_t*>(base);
+  // zeroed region first: look-back states + counters
+  w.off_states = b;
+  w.off_counter = reinterpret_cast<unsigned long long*>(b + otiles);
+  w.dec_states = b + otiles + 1;
+  w.dec_counter = reinterpret_cast<unsigned long long*>(b + otiles + 1 + dtiles);
+  w.zero_bytes = (otiles + dtiles + 2) * sizeof(uint64_t);
+  w.offsets = b + otiles + dtiles + 2;
+  w.total = w.zero_bytes + (chunked ? (nchunks + 1) * sizeof(uint64_t) : 0) + 256;
+  return w;
+}
+
+template <int FMT, int CB, int POSB>
+void launch_decode(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+  decode_kernel<FMT, CB, POSB, kDecodeItems><<<static_cast<unsigned>(a.num_tiles), kThreads, 0, s>>>(p, a);
+}
+template <int FMT, int CB>
+void dec_pos(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+  switch (posb) {
+    case 0: launch_decode<FMT, CB, 0>(p, a, s); break;
+    case 1: launch_decode<FMT, CB, 1>(p, a, s); break;
+    case 2: launch_decode<FMT, CB, 2>(p, a, s); break;
+    default: launch_decode<FMT, CB, 4>(p, a, s); break;
+  }
+}
+template <int FMT>
+void dec_cb(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+  if (p.code_bits == 4) dec_pos<FMT, 4>(posb, p, a, s);
+  else dec_pos<FMT, 3>(posb, p, a, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sz_record_cuda(cudaError_t e);
+int sz_check_params(const sz_params* p, int decode_side);
+
+size_t sz_decode_workspace_bytes(uint64_t n, uint64_t m, const sz_params* p) {
+  (void)m;
+  if (!p || p->fmt > SZ_E4M3 || p->chunk_size == 0) return 0;
+  return carve(nullptr, n, p).total;
+}
+
+int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
+              sz_decode_status* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  if (int rc = sz_check_params(p, 1)) return rc;
+  if (!in || !d_words_out || !d_status || in->n_elements == 0) return SZ_ECONFIG;
+  if (!in->d_n_escapes && in->n_escapes > in->n_elements) return SZ_ECONFIG;
+  const uint64_t n = in->n_elements, m = in->d_n_escapes ? n : in->n_escapes;
+  if ((reinterpret_cast<uintptr_t>(d_words_out) & 31) ||
+      (reinterpret_cast<uintptr_t>(in->d_codes) & 15) || (reinterpret_cast<uintptr_t>(in->d_sm) & 15))
+    return SZ_EALIGN;
+  if (ws_bytes < sz_decode_workspace_bytes(n, m, p)) return SZ_EWORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool chunked = !p->sentinel && !p->abs32;
+  const int sm_bits = p->fmt == SZ_BF16 ? 8 : (p->fmt == SZ_E5M2 ? 3 : 4);
+  DecodeWs w = carve(d_ws, n, p);
+  const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size : 0;
+  if (chunked && in->n_counts != nchunks) return SZ_ECONFIG;  // host raises first
+  if (!in->d_n_escapes && m && (!in->d_values || (!p->sentinel && !in->d_positions)))
+    return SZ_ECONFIG;
+
+  cudaError_t e = cudaMemsetAsync(d_status, 0, sizeof(sz_decode_status), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_ws, 0, w.zero_bytes, s);
+  if (e != cudaSuccess) return sz_record_cuda(e);
+
+  if (chunked) {
+    OffsetsArgs oa{};
+    oa.m_ptr = in->d_n_escapes;
+    oa.counts = in->d_counts;
+    oa.n_counts = nchunks;
+    oa.m = m;
+    oa.offsets = w.offsets;
+    oa.states = w.off_states;
+    oa.tile_counter = w.off_counter;
+    oa.num_tiles = offsets_tiles(nchunks);
+    oa.status = d_status;
+    offsets_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(oa);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return sz_record_cuda(e);
+  }
+
+  DecodeArgs a{};
+  a.m_ptr = in->d_n_escapes;
+  a.codes = static_cast<const uint8_t*>(in->d_codes);
+  a.sm = static_cast<const uint8_t*>(in->d_sm);
+  a.offsets = w.offsets;
+  a.positions = in->d_positions;
+  a.values = in->d_values;
+  a.n = n;
+  a.m = m;
+  a.out = static_cast<uint8_t*>(d_words_out);
+  a.status = d_status;
+  a.states = w.dec_states;
+  a.tile_counter = w.dec_counter;
+  a.num_tiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
+  a.n_chunks = nchunks;
+  a.codes_len = (n * p->code_bits + 7) / 8;
+  a.sm_len = (n * sm_bits + 7) / 8;
+  a.chunk = p->chunk_size;
+  a.chunk_shift = (p->chunk_size & (p->chunk_size - 1)) == 0 ? __builtin_ctz(p->chunk_size) : -1;
+  const int posb = p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
+  switch (p->fmt) {
+    case SZ_BF16: dec_cb<SZ_BF16>(posb, *p, a, s); break;
+    case SZ_E5M2: dec_cb<SZ_E5M2>(posb, *p, a, s); break;
+    default: dec_cb<SZ_E4M3>(posb, *p, a, s); break;
+  }
+  e = cudaGetLastError();
+  return e == cudaSuccess ? SZ_OK : sz_record_cuda(e);
+}
+
+int sz_check_values(const uint8_t* d_values, uint64_t m, const sz_params* p,
+                    sz_decode_status* d_status, void* stream) {
+  if (int rc = sz_check_params(p, 1)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(d_status, 0, sizeof(sz_decode_status), s);
+  if (e != cudaSuccess) return sz_record_cuda(e);
+  if (!m) return SZ_OK;
+  uint64_t g = (m + kThreads - 1) / kThreads;
+  if (g > 148 * 8) g = 148 * 8;
+  check_values_kernel<<<static_cast<unsigned>(g), kThreads, 0, s>>>(d_values, m, *p, d_status);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? SZ_OK : sz_record_cuda(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+"""GPU parity: the sm_100a kernels against the reference's golden vectors and
+the CPU oracle, byte for byte (sections) and bit for bit (decoded words)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sz_oracle as O
+from sz_testutil import golden, golden_case_ids, oracle_params
+
+pytestmark = pytest.mark.gpu
+
+SECTIONS = ("chunk_counts", "packed_codes", "sign_mantissa", "escape_positions",
+            "escape_values")
+
+
+def sz():
+    import paper_2605_01708_b200 as m
+    return m
+
+
+def make_config(case, pinned=True):
+    m = sz()
+    fmt = [m.ElementFormat.BF16, m.ElementFormat.FP8_E5M2, m.ElementFormat.FP8_E4M3][case["fmt"]]
+    mode = m.CodebookMode.TOP15_SENTINEL if case["sentinel"] else m.CodebookMode.TOPK_EXPLICIT
+    pos = m.PositionMode.ABSOLUTE_32 if case["abs32"] else m.PositionMode.CHUNK_RELATIVE
+    book = (m.ExponentCodebook(fmt, tuple(case["book"]), case["code_bits"], mode)
+            if pinned and case["pinned"] else None)
+    return fmt, m.CodecConfig(fmt, case["code_bits"], mode, case["chunk"], pos, book)
+
+
+@pytest.mark.parametrize("device_api", [False, True], ids=["host-api", "device-api"])
+@pytest.mark.parametrize("cid", golden_case_ids())
+def test_encode_decode_matches_reference(cid, device_api):
+    m = sz()
+    g = golden()
+    case = g.case(cid)
+    words = g.arr(cid, "words")
+    fmt, cfg = make_config(case)
+    src = torch.from_numpy(words.copy()).cuda() if device_api else words
+    stream = m.RawTensorStream(fmt, src)
+    enc = m.encode(stream, cfg)
+    assert enc.n_escapes == case["m"]
+    assert list(enc.codebook.entries) == case["book"]
+    assert enc.on_device == device_api
+    got = dict(enc.section_bytes())
+    for name in SECTIONS:
+        assert got[name] == g.arr(cid, name).tobytes(), name
+    assert enc.payload_nbytes == case["payload_nbytes"]
+    dec = m.decode(enc, cfg, enc.codebook)
+    out = dec.words.cpu().numpy() if device_api else dec.words
+    assert np.array_equal(out, words)
+    quad = m.encode_quad(stream, cfg)
+    assert dict(quad.section_bytes()) == got
+
+
+@pytest.mark.parametrize("cid", golden_case_ids())
+def test_histogram_matches_reference(cid):
+    m = sz()
+    g = golden()
+    case = g.case(cid)
+    fmt, _ = make_config(case)
+    stats = m.build_histogram(m.RawTensorStream(fmt, g.arr(cid, "words")))
+    assert np.array_equal(stats.counts, g.arr(cid, "hist"))
+    assert m.entropy_bits(stats) == pytest.approx(case["entropy"], abs=1e-12)
+
+
+@pytest.mark.parametrize("verdict", golden().corruptions, ids=lambda v: v["id"])
+def test_corruption_verdicts_match_reference(verdict):
+    m = sz()
+    g = golden()
+    words = g.arr("corrupt", "words")
+    stream = m.RawTensorStream(m.ElementFormat.BF16, words)
+    book = m.select_codebook(m.build_histogram(stream), 4, m.CodebookMode.TOPK_EXPLICIT)
+    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
+    pre = f"corrupt_{verdict['id']}"
+    streams = m.EncodedStreams(
+        verdict["n"], verdict["m"], g.arr(pre, "packed_codes").tobytes(),
+        g.arr(pre, "sign_mantissa").tobytes(), g.arr(pre, "chunk_counts"),
+        g.arr(pre, "escape_positions"), g.arr(pre, "escape_values"), book)
+    if verdict["raised"] is None:
+        assert np.array_equal(m.decode(streams, cfg, book).words, words)
+        return
+    with pytest.raises(m.CorruptionError) as exc:
+        m.decode(streams, cfg, book)
+    assert exc.value.chunk == verdict["chunk"]
+
+
+@pytest.mark.parametrize("fmt_id", [0, 1, 2])
+def test_split_reconstruct_exhaustive(fmt_id):
+    m = sz()
+    fmt = list(m.ElementFormat)[fmt_id]
+    words = np.arange(1 << fmt.word_bits, dtype=fmt.word_dtype)
+    e, a = m.split_fields(words, fmt)
+    oe, oa = O.split(words, fmt_id)
+    assert np.array_equal(e, oe) and np.array_equal(a, oa)
+    assert np.array_equal(m.reconstruct(m.SplitFields(e, a), fmt), words)
+
+
+@pytest.mark.parametrize("bits", [3, 4])
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 9, 1000, 4097])
+def test_pack_unpack_codes(bits, n):
+    m = sz()
+    rng = np.random.default_rng(n * 10 + bits)
+    codes = rng.integers(0, 1 << bits, size=n, dtype=np.uint8)
+    packed = m.pack_codes(codes, bits)
+    assert packed == O.pack_le(codes, bits)
+    assert np.array_equal(m.unpack_codes(packed, n, bits), codes)
+    with pytest.raises(m.CodeRangeError):
+        m.pack_codes(np.array([1 << bits], dtype=np.uint8), bits)
+
+
+def test_known_answers():
+    m = sz()
+    # test_formats.py / test_codec.py known answers
+    assert m.pack_codes([1, 2], 4) == bytes([0x21])
+    assert m.pack_codes([7] * 8, 3) == b"\xff\xff\xff"
+    book = m.ExponentCodebook(m.ElementFormat.BF16, (0x7F,), 4, m.CodebookMode.TOPK_EXPLICIT)
+    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
+    streams = m.EncodedStreams(2, 0, bytes([0]), bytes([0x00, 0x80]),
+                               np.zeros(1, np.uint32), np.zeros(0, np.uint16),
+                               np.zeros(0, np.uint8), book)
+    assert m.decode(streams, cfg, book).words.tolist() == [0x3F80, 0xBF80]
+
+
+def test_single_escape_location():
+    # test_codec.py:84-101
+    m = sz()
+    words = O.exact_stream(0, 1024, 0.0, 6, O.BF16_BOOK, O.BF16_ESC)
+    book_words = words.copy()
+    words[700] = O.join(np.array([0x10]), np.array([0x55]), 0)[0]
+    stream = m.RawTensorStream(m.ElementFormat.BF16, words)
+    book = m.select_codebook(m.build_histogram(m.RawTensorStream(m.ElementFormat.BF16, book_words)),
+                             4, m.CodebookMode.TOPK_EXPLICIT)
+    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
+    enc = m.encode(stream, cfg)
+    assert enc.n_escapes == 1 and enc.chunk_counts.tolist() == [1]
+    assert enc.escape_positions.tolist() == [700] and enc.escape_values.tolist() == [0x10]
+    assert enc.packed_codes[350] & 0x0F == 0
+    assert np.array_equal(m.decode(enc, cfg, enc.codebook).words, words)
+    chunks = list(enc.escape_chunks())
+    assert chunks[0].count == 1 and chunks[0].index == 0
+
+
+def test_zero_coverage_all_escape():
+    m = sz()
+    words = O.exact_stream(0, 4096, 0.0, 14, O.BF16_BOOK, O.BF16_ESC)
+    book = m.ExponentCodebook(m.ElementFormat.BF16, (1, 2), 4, m.CodebookMode.TOPK_EXPLICIT)
+    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
+    stream = m.RawTensorStream(m.ElementFormat.BF16, words)
+    enc = m.encode(stream, cfg, capacity=16)  # forces the overflow-retry protocol
+    assert enc.n_escapes == 4096
+    assert np.array_equal(m.decode(enc, cfg, book).words, words)
+
+
+def test_errors_and_empty():
+    m = sz()
+    with pytest.raises(m.EmptyInputError):
+        m.encode(m.RawTensorStream(m.ElementFormat.BF16, np.zeros(0, np.uint16)),
+                 m.CodecConfig(m.ElementFormat.BF16))
+    with pytest.raises(m.ConfigError):
+        m.encode(m.RawTensorStream(m.ElementFormat.FP8_E5M2, np.zeros(4, np.uint8)),
+                 m.CodecConfig(m.ElementFormat.BF16))
+    with pytest.raises(m.EmptyInputError):
+        m.build_histogram(m.RawTensorStream(m.ElementFormat.BF16, np.zeros(0, np.uint16)))
+
+
+@pytest.mark.parametrize("fmt_id,n,rate,chunk", [
+    (0, 1 << 22, 0.0016, 1024), (0, (1 << 22) + 777, 0.0123, 256), (0, 3_000_001, 0.05, 4096),
+    (1, 1 << 22, 0.0016, 1024), (1, (1 << 22) + 5, 0.0123, 65536), (2, 1 << 21, 0.05, 1024),
+])
+def test_large_streams_match_oracle(fmt_id, n, rate, chunk):
+    m = sz()
+    bk, esc = {0: (O.BF16_BOOK, O.BF16_ESC), 1: (O.E5M2_BOOK, O.E5M2_ESC),
+               2: (O.E4M3_BOOK, O.E4M3_ESC)}[fmt_id]
+    words = O.exact_stream(fmt_id, n, rate, 42 + fmt_id, bk, esc)
+    book = tuple(e for e, _ in bk)
+    fmt = list(m.ElementFormat)[fmt_id]
+    cb = 4 if len(book) == 16 else 3
+    cfg = m.CodecConfig(fmt, cb, chunk_size=chunk,
+                        codebook=m.ExponentCodebook(fmt, book, cb, m.CodebookMode.TOPK_EXPLICIT))
+    stream = m.RawTensorStream(fmt, torch.from_numpy(words).cuda())
+    enc = m.encode(stream, cfg)
+    ref = O.encode(words, O.Params(fmt_id, cb, False, chunk, False), book)
+    assert enc.n_escapes == ref["m"] == round(rate * n)
+    assert dict(enc.section_bytes())["packed_codes"] == ref["packed_codes"]
+    assert [b for _, b in enc.section_bytes()] == O.section_bytes(ref)
+    dec = m.decode(enc, cfg, enc.codebook)
+    assert m.compare_streams(stream, dec).ok
+
+
+def test_compare_streams_reports_first_mismatch():
+    m = sz()
+    a = np.arange(100_000, dtype=np.uint16)
+    b = a.copy()
+    b[[777, 5000, 99_999]] ^= 1
+    r = m.compare_streams(m.RawTensorStream(m.ElementFormat.BF16, a),
+                          m.RawTensorStream(m.ElementFormat.BF16, b))
+    assert (r.ok, r.mismatch_count, r.first_mismatch_index) == (False, 3, 777)
+    r = m.compare_streams(m.RawTensorStream(m.ElementFormat.FP8_E5M2, a.view(np.uint8)),
+                          m.RawTensorStream(m.ElementFormat.FP8_E5M2, b.view(np.uint8)))
+    assert (r.mismatch_count, r.first_mismatch_index) == (3, 2 * 777)
+
+
+def test_coverage_by_group():
+    m = sz()
+    clean = O.exact_stream(0, 10_000, 0.0, 4, O.BF16_BOOK, O.BF16_ESC)
+    dirty = O.exact_stream(0, 10_000, 0.0123, 5, O.BF16_BOOK, O.BF16_ESC)
+    stream = m.RawTensorStream(m.ElementFormat.BF16, np.concatenate([clean, dirty]))
+    book = m.select_codebook(m.build_histogram(m.RawTensorStream(m.ElementFormat.BF16, clean)),
+                             4, m.CodebookMode.TOPK_EXPLICIT)
+    assert m.coverage_by_group(stream, 10_000, book).tolist() == [1.0, 0.9877]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_lengths_roundtrip(seed):
+    # hypothesis-style sweep of ragged lengths (test_codec.py:256-260)
+    m = sz()
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 40_000))
+    fmt_id = seed % 3
+    words = O.random_words(fmt_id, n, seed)
+    fmt = list(m.ElementFormat)[fmt_id]
+    stream = m.RawTensorStream(fmt, words)
+    for cfg in (m.CodecConfig(fmt), m.CodecConfig(fmt, 3, chunk_size=int(rng.integers(1, 3000))),
+                m.CodecConfig(fmt, mode=m.CodebookMode.TOP15_SENTINEL),
+                m.CodecConfig(fmt, position_mode=m.PositionMode.ABSOLUTE_32)):
+        enc = m.encode(stream, cfg)
+        p = O.Params(fmt_id, cfg.code_bits, cfg.sentinel, cfg.chunk_size, cfg.abs32)
+        ref = O.encode(words, p, enc.codebook.entries)
+        assert [b for _, b in enc.section_bytes()] == O.section_bytes(ref)
+        assert m.verify_roundtrip(stream, cfg).ok
