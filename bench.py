@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""SplitZip-B200 benchmark — one JSON line from rank 0.
+
+A *step* is one pass of the codec hot path over the batch: encode (K2) then
+decode (K3+K4) of the rank's synthetic KV shard, inputs resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4]
+                  [--chunk C] [--escape-rate E] [--impl ours|reference]
+
+Workloads (BASELINE.json configs):
+  c2  Llama-3.1-8B BF16 KV at 32K tokens per GPU (32 layers x K/V x 32768
+      tokens x 8 KV heads x 128) = 2^31 words = 4 GiB.  Default.  Under
+      torchrun every rank holds its own 4 GiB shard (weak scaling).
+  c3  the same shape as FP8 E5M2 (2 GiB per GPU).
+  c4  Llama-3-70B BF16 KV at 128K tokens (80 layers x K/V x 131072 x 8 x 128,
+      40 GiB) sharded by KV head over the N ranks (strong scaling).
+Inputs (4 GiB) are 32x larger than L2 (126 MB), so no L2 flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BOOK16_BF16 = tuple((0x70 + i, 0.72 ** i) for i in range(16))
+ESC_BF16 = tuple(range(0x10, 0x18))
+BOOK16_E5M2 = tuple((8 + i, 0.72 ** i) for i in range(16))
+ESC_E5M2 = (0, 1, 2, 3, 28, 29, 30, 31)
+METRIC = "encode/decode GB/s of BF16 KV input per B200 (and 8-GPU aggregate); compression ratio"
+PAPER_B200 = {"encode": 637.9, "decode": 2607.4}
+FALLBACK_HBM = 6650.0                              # B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--chunk", type=int, default=1024)
+    ap.add_argument("--escape-rate", type=float, default=0.0016)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=20260517)
+    return ap.parse_args()
+
+
+def workload(name: str, world: int) -> dict:
+    if name == "c4":
+        heads = 8
+        if heads % world:
+            raise SystemExit(f"c4 shards 8 KV heads; {world} ranks do not divide it")
+        n = 80 * 2 * 131072 * (heads // world) * 128
+        return dict(name="c4", fmt_id=0, n=n, scaling="strong",
+                    desc=f"Llama-3-70B BF16 KV 128K tokens, KV heads sharded {heads // world}/rank")
+    n = 32 * 2 * 32768 * 8 * 128
+    if name == "c3":
+        return dict(name="c3", fmt_id=1, n=n, scaling="weak",
+                    desc="Llama-3.1-8B FP8-E5M2 KV 32K tokens per GPU")
+    return dict(name="c2", fmt_id=0, n=n, scaling="weak",
+                desc="Llama-3.1-8B BF16 KV 32K tokens per GPU (32x2x32768x8x128)")
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled while the GPU works."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [l.split(", ") for l in self.lines if l.count(",") >= 7]
+        busy = [r for r in rows if r[3].strip().isdigit() and int(r[3]) > 0] or rows
+        sm = [int(r[1]) for r in busy if r[1].strip().isdigit()]
+        mx = [int(r[2]) for r in rows if r[2].strip().isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[4 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows), "samples_busy": len(busy)}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from oracle import cpu_bench
+    wl = workload(args.workload, world)
+    fmt = wl["fmt_id"]
+    book_w, esc = (BOOK16_BF16, ESC_BF16) if fmt == 0 else (BOOK16_E5M2, ESC_E5M2)
+    book = tuple(e for e, _ in book_w)
+    workers = max(1, min(os.cpu_count() or 1, 32))
+    per = 1 << 22
+    for _ in range(args.warmup):
+        cpu_bench.roundtrip_throughput(fmt, book, book_w, esc, args.escape_rate, args.chunk,
+                                       per, workers, 1, seed=args.seed)
+    total_b = total_t = 0.0
+    for s in range(args.steps):
+        r = cpu_bench.roundtrip_throughput(fmt, book, book_w, esc, args.escape_rate, args.chunk,
+                                           per, workers, 1, seed=args.seed + s)
+        total_b += r["bytes"]
+        total_t += r["wall_s"]
+    gbs = total_b / total_t / 1e9
+    sample = (f"{workers} procs x 2^22 words per step (chunk-aligned shards of the {wl['name']} "
+              "workload's exponent distribution), numpy oracle restating the reference codec")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_t / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": wl["scaling"], "vs_baseline": None, "dtype": "u16" if fmt == 0 else "u8",
+        "data": "synthetic", "config": {"workload": wl["desc"], "chunk": args.chunk,
+                                        "escape_rate": args.escape_rate},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_01708_b200 as sz
+    from paper_2605_01708_b200 import _native as N
+    from paper_2605_01708_b200.calibration import build_histogram_device
+    from paper_2605_01708_b200.engine import DeviceCodec, synth_kv
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    wl = workload(args.workload, world)
+    fmt = [sz.ElementFormat.BF16, sz.ElementFormat.FP8_E5M2][wl["fmt_id"]]
+    book_w, esc = (BOOK16_BF16, ESC_BF16) if wl["fmt_id"] == 0 else (BOOK16_E5M2, ESC_E5M2)
+    n = wl["n"]
+    raw = n * fmt.word_nbytes
+
+    # ---- input shard, generated on the device (K8)
+    words = synth_kv(n, fmt, args.seed + rank, book_w, esc, args.escape_rate)
+
+    # ---- calibration: K1 histogram per rank, NCCL all-reduce = merge_stats
+    counts = build_histogram_device(words, fmt)
+    if world > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    stats = sz.CalibrationStats(fmt, counts.cpu().numpy(), n * world)
+    book = sz.select_codebook(stats, 4, sz.CodebookMode.TOPK_EXPLICIT)
+    cfg = sz.CodecConfig(fmt, 4, chunk_size=args.chunk, codebook=book)
+    eng = DeviceCodec(cfg, book, n)
+    m = eng.ensure_capacity(words)
+
+    # ---- verify bitwise before timing (K4 + K7)
+    eng.decode()
+    eng.check_status()
+    cmp = eng.compare(words, eng.out).cpu().numpy()
+    assert int(cmp[0]) == 0, f"rank {rank}: roundtrip mismatch count {int(cmp[0])}"
+    payload = eng.payload_nbytes(m)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        eng.encode(words)
+        eng.decode()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+
+    # ---- timed region: exactly K steps
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(K):
+        ev[k][0].record(stream)
+        eng.encode(words)
+        ev[k][1].record(stream)
+        eng.decode()
+        ev[k][2].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    enc_ms = sum(ev[k][0].elapsed_time(ev[k][1]) for k in range(K))
+    dec_ms = sum(ev[k][1].elapsed_time(ev[k][2]) for k in range(K))
+    tot_ms = ev[0][0].elapsed_time(ev[K - 1][2])
+    tot_ms = max_over_ranks(tot_ms)
+    enc_ms = max_over_ranks(enc_ms)
+    dec_ms = max_over_ranks(dec_ms)
+    eng.check_status()
+
+    # ---- e2e through the public API with pinned host buffers
+    host = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
+    host.copy_(words)
+    torch.cuda.synchronize()
+    e2e_steps = max(1, args.e2e_steps)
+    h2d = d2h = 0
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        enc = sz.encode(sz.RawTensorStream(fmt, host), cfg)
+        dec = sz.decode(enc, cfg, book)
+        h2d += raw + enc.payload_nbytes
+        d2h += enc.payload_nbytes + raw
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    assert np.array_equal(dec.words[:1 << 16], host[:1 << 16].numpy())
+    clocks = sampler.stop()
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = measured_peak()
+    # algorithmic bytes of one encode (or decode) launch: the raw words read
+    # (written) plus every payload section written (read) — DESIGN.md §4.
+    alg_bytes = raw + payload
+    enc_launch_ms = enc_ms / K
+    dec_launch_ms = dec_ms / K
+    dominant = "encode" if enc_launch_ms >= dec_launch_ms else "decode"
+    dom_ms = max(enc_launch_ms, dec_launch_ms)
+    achieved = alg_bytes / (dom_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_traffic_{wl['name']}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"{dominant}_kernel_dram_bytes")
+        except Exception:
+            traffic = None
+
+    value = world * raw * K / (tot_ms / 1e3) / 1e9
+    enc_gbs = world * raw * K / (enc_ms / 1e3) / 1e9
+    dec_gbs = world * raw * K / (dec_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round(tot_ms / K, 4),
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
+        "dtype": "u16" if fmt.word_bits == 16 else "u8", "data": "synthetic",
+        "config": {"workload": wl["desc"], "elements_per_gpu": n, "chunk": args.chunk,
+                   "code_bits": 4, "escape_rate_target": args.escape_rate,
+                   "escape_rate": round(m / n, 6), "codebook": list(book.entries),
+                   "l2": "inputs (>=2 GiB/rank) exceed the 126 MB L2; no flush needed",
+                   "step": "encode (K2) + decode (K3+K4), round trip"},
+        "encode_gbs": round(enc_gbs, 2), "decode_gbs": round(dec_gbs, 2),
+        "compression_ratio": round(raw / payload, 5),
+        "vs_paper_b200": {"encode": round(enc_gbs / world / PAPER_B200["encode"], 3),
+                          "decode": round(dec_gbs / world / PAPER_B200["decode"], 3)},
+        "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "encode_frac": round(alg_bytes / (enc_launch_ms / 1e3) / 1e9 / peak, 4),
+                     "decode_frac": round(alg_bytes / (dec_launch_ms / 1e3) / 1e9 / peak, 4)},
+        "e2e": {"value": round(world * raw * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
+                "api": "paper_2605_01708_b200.encode/decode on pinned host words"},
+        "gpu_launches": K * (3 + (1 if fmt.exp_bits != 8 else 0)),
+        "clocks": clocks,
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m) -> dict:
+    """Oracle on host cores (bounded sample) + oracle slice-parity check."""
+    import numpy as np
+    from oracle import cpu_bench
+
+    fmt_id = wl["fmt_id"]
+    # parity: oracle on a chunk-aligned 2^20-word prefix vs the GPU sections
+    pre = 1 << 20
+    w = words[:pre].cpu().numpy()
+    streams = eng.streams(m)
+    k = pre // args.chunk
+    counts = streams.chunk_counts[:k].cpu().numpy()
+    mm = int(counts.sum())
+    sec = {"packed_codes": streams.packed_codes[:pre // 2].cpu().numpy().tobytes(),
+           "sign_mantissa": streams.sign_mantissa[:pre * wl_sm_bits(fmt_id) // 8].cpu().numpy().tobytes(),
+           "chunk_counts": counts,
+           "escape_positions": streams.escape_positions[:mm].cpu().numpy(),
+           "escape_values": streams.escape_values[:mm].cpu().numpy()}
+    ok = cpu_bench.slice_parity(w, fmt_id, book.entries, args.chunk, sec)
+    assert ok, "GPU sections differ from the oracle on the verification slice"
+    workers = max(1, min(os.cpu_count() or 1, 32))
+    per = 1 << 22
+    r = cpu_bench.roundtrip_throughput(fmt_id, book.entries, book_w, esc, args.escape_rate,
+                                       args.chunk, per, workers, 1, seed=args.seed)
+    return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": workers, "kind": "port",
+            "sample": f"{workers} procs x 2^22 words, one encode+decode each "
+                      f"({r['cpu_seconds']:.1f} CPU-s); numpy oracle of the reference codec",
+            "encode_gbs": round(r["encode_gbs"], 4), "decode_gbs": round(r["decode_gbs"], 4),
+            "slice_parity": "2^20-word prefix: GPU sections == oracle"}
+
+
+def wl_sm_bits(fmt_id: int) -> int:
+    return {0: 8, 1: 3, 2: 4}[fmt_id]
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
