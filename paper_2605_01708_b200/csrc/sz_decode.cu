@@ -439,6 +439,290 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ------------------------------------------------------------------ K4 (persistent)
+// Explicit modes (chunk-relative and abs32).  Same warp-specialised shape as
+// the encoder: warp 8 streams each tile's code and sign|mantissa planes into a
+// shared-memory ring with TMA bulk copies; warp 9 stages the tile's escapes
+// (bitmap + raw values in smem) and runs every per-escape check; warps 0-7
+// decode slots from smem and write 256-bit stores.  No CTA-wide barriers in
+// steady state — only mbarrier hand-offs.
+constexpr int kDecStages = 4;
+constexpr int kDecItems = 2;
+constexpr int kDecSlots = kDecItems * kThreads;        // 512 slots per tile
+constexpr int kDecThreads = kThreads + 64;
+constexpr int kDecPlaneBytes = kDecSlots * 16;         // max bytes of one plane per tile
+constexpr int kDecOffStage = 1024;
+
+template <int FMT>
+struct DecSmem {
+  static constexpr int EPV = kEpv<FMT>;
+  static constexpr int TILE = kDecSlots * EPV;
+  alignas(128) uint8_t codes[kDecStages][kDecPlaneBytes];
+  alignas(128) uint8_t sm[kDecStages][kDecPlaneBytes];
+  alignas(16) uint8_t vals[kDecStages][TILE];
+  uint32_t bitmap[kDecStages][TILE / 32];
+  uint64_t off[kDecOffStage + 1];
+  uint32_t lut2[256];
+  uint64_t meta[kDecStages];
+  uint64_t full[kDecStages];
+  uint64_t staged[kDecStages];
+  uint64_t empty[kDecStages];
+};
+
+template <int FMT, int CB, int POSB>
+__global__ void __launch_bounds__(kDecThreads, 2)
+    decode_persistent(const __grid_constant__ sz_params p, const DecodeArgs a) {
+  constexpr int EPV = kEpv<FMT>;
+  constexpr int G = EPV / 4;
+  constexpr int WB = Fmt<FMT>::kWordBytes;
+  constexpr int SMB = Fmt<FMT>::kSmBits;
+  constexpr int CBYTES = EPV * CB / 8;
+  constexpr int SBYTES = EPV * SMB / 8;
+  constexpr int CWORDS = (CBYTES + 3) / 4;
+  constexpr int SWORDS = (SBYTES + 3) / 4;
+  constexpr uint64_t TILE = static_cast<uint64_t>(kDecSlots) * EPV;
+  constexpr bool ABS = POSB == 4;
+  constexpr int LUT2 = CB == 4 ? 256 : 64;
+  constexpr uint32_t kCodeMask = (1u << CB) - 1;
+  using Smem = DecSmem<FMT>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
+  for (int i = tid; i < LUT2; i += kDecThreads) {
+    const uint32_t c0 = i & kCodeMask, c1 = (i >> CB) & kCodeMask;
+    const uint32_t bad = (c0 >= p.n_entries) | ((c1 >= p.n_entries) << 1);
+    S.lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kDecStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.staged[s], 1);
+      mbar_init(&S.empty[s], kThreads);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t s = it % kDecStages, ph = (it / kDecStages) & 1;
+        mbar_wait(&S.empty[s], ph ^ 1);
+        const uint64_t tile = atomicAdd(a.tile_counter, 1ull);
+        if (tile >= a.num_tiles) {
+          S.meta[s] = ~0ull;
+          mbar_arrive(&S.full[s]);
+          break;
+        }
+        S.meta[s] = tile;
+        const uint64_t e0 = tile * TILE;
+        const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
+        const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
+        const uint32_t sbytes = (full_slots * SBYTES) & ~15u;
+        mbar_arrive_tx(&S.full[s], cbytes + sbytes);
+        if (cbytes) tma_load_1d(S.codes[s], a.codes + e0 * CB / 8, cbytes, &S.full[s]);
+        if (sbytes) tma_load_1d(S.sm[s], a.sm + e0 * SMB / 8, sbytes, &S.full[s]);
+      }
+    }
+    return;
+  }
+
+  if (warp == kWarps + 1) {
+    // ------------------------------------------------------------ escape stager
+    const uint32_t exp_bins = 1u << Fmt<FMT>::kExpBits;
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t s = it % kDecStages, ph = (it / kDecStages) & 1;
+      mbar_wait(&S.full[s], ph);
+      const uint64_t tile = S.meta[s];
+      if (tile == ~0ull) break;
+      const uint64_t s0 = tile * TILE, s1 = min(s0 + TILE, n);
+#pragma unroll
+      for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
+      // per-ordinal checks independent of the counts, spread evenly over tiles
+      {
+        const uint64_t q = (m + a.num_tiles - 1) / a.num_tiles;
+        const uint64_t o0 = tile * q, o1 = min(o0 + q, m);
+        for (uint64_t o = o0 + lane; o < o1; o += 32) {
+          const uint32_t v = a.values[o];
+          if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+          else if (!(p.enc_lut[v] & 0x10))
+            record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+          if constexpr (ABS) {
+            const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
+            const uint32_t pv = pos[o];
+            if (pv >= n) record_first(&a.status->first_inv[SZ_DEC_ABS_PAST_END], o);
+            if (o > 0 && pv <= pos[o - 1])
+              record_first(&a.status->first_inv[SZ_DEC_ABS_NOT_INC], o);
+          }
+        }
+      }
+      if (tile == a.num_tiles - 1 && lane == 0) {
+        const uint32_t cbits = static_cast<uint32_t>((n * CB) & 7);
+        if (cbits && (a.codes[a.codes_len - 1] >> cbits))
+          record_first(&a.status->first_inv[SZ_DEC_CODE_PAD], 0);
+        if constexpr (SMB != 8) {
+          const uint32_t sbits = static_cast<uint32_t>((n * SMB) & 7);
+          if (sbits && (a.sm[a.sm_len - 1] >> sbits))
+            record_first(&a.status->first_inv[SZ_DEC_SM_PAD], 0);
+        }
+      }
+      __syncwarp();
+      if constexpr (ABS) {
+        const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
+        const uint64_t lo = warp_lower_bound(pos, m, s0);
+        const uint64_t hi = max(lo, warp_lower_bound(pos, m, s1));
+        for (uint64_t o = lo + lane; o < hi; o += 32) {
+          const uint64_t idx = pos[o];
+          if (idx >= s0 && idx < s1) {
+            const uint32_t rel = static_cast<uint32_t>(idx - s0);
+            atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
+            S.vals[s][rel] = a.values[o];
+          }
+        }
+      } else {
+        const uint64_t ka = s0 / a.chunk, kb = (s1 - 1) / a.chunk;
+        const uint64_t nk = kb - ka + 2;
+        const bool staged = nk <= kDecOffStage + 1;
+        if (staged)
+          for (uint64_t i = lane; i < nk; i += 32) S.off[i] = a.offsets[ka + i];
+        __syncwarp();
+        const uint64_t* off = staged ? S.off : a.offsets + ka;
+        const uint64_t o_lo = min(off[0], m), o_hi = min(off[nk - 1], m);
+        for (uint64_t o = o_lo + lane; o < o_hi; o += 32) {
+          uint64_t lo = 0, hi = nk - 1;
+          while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (off[mid] <= o) lo = mid; else hi = mid;
+          }
+          const uint64_t pv = load_pos<POSB>(a.positions, o);
+          if (pv >= a.chunk) {
+            record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+            continue;
+          }
+          const uint64_t idx = (ka + lo) * a.chunk + pv;
+          if (idx >= n) {
+            record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+            continue;
+          }
+          if (o > off[lo] && load_pos<POSB>(a.positions, o - 1) >= pv)
+            record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+          if (idx >= s0 && idx < s1) {
+            const uint32_t rel = static_cast<uint32_t>(idx - s0);
+            atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
+            S.vals[s][rel] = a.values[o];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.staged[s]);
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ decode warps
+  const bool check_range = p.n_entries < (1u << CB);
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t s = it % kDecStages, ph = (it / kDecStages) & 1;
+    mbar_wait(&S.full[s], ph);
+    const uint64_t tile = S.meta[s];
+    if (tile == ~0ull) break;
+    const uint64_t tile_e0 = tile * TILE;
+    const uint32_t full_slots = static_cast<uint32_t>(min(n - tile_e0, TILE) / EPV);
+    const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
+    const uint32_t sbytes = (full_slots * SBYTES) & ~15u;
+    mbar_wait(&S.staged[s], ph);
+#pragma unroll
+    for (int i = 0; i < kDecItems; ++i) {
+      const uint32_t slot = i * kThreads + tid;
+      const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
+      if (e0 >= n) continue;
+      const int nv = e0 + EPV <= n ? EPV : static_cast<int>(n - e0);
+      uint32_t cw[CWORDS], sw[SWORDS];
+      if ((slot + 1) * CBYTES <= cbytes && (slot + 1) * SBYTES <= sbytes) {
+        const uint8_t* cp = S.codes[s] + slot * CBYTES;
+        const uint8_t* sp = S.sm[s] + slot * SBYTES;
+        if constexpr (CBYTES == 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(cp);
+          cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
+        } else if constexpr (CBYTES == 8) {
+          const uint2 v = *reinterpret_cast<const uint2*>(cp);
+          cw[0] = v.x; cw[1] = v.y;
+        } else if constexpr (CBYTES == 12) {
+          const uint32_t* q = reinterpret_cast<const uint32_t*>(cp);
+          cw[0] = q[0]; cw[1] = q[1]; cw[2] = q[2];
+        } else {
+          const uint16_t* q = reinterpret_cast<const uint16_t*>(cp);
+          cw[0] = q[0] | (static_cast<uint32_t>(q[1]) << 16);
+          cw[1] = q[2];
+        }
+        if constexpr (SBYTES == 16) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sp);
+          sw[0] = v.x; sw[1] = v.y; sw[2] = v.z; sw[3] = v.w;
+        } else {
+          const uint32_t* q = reinterpret_cast<const uint32_t*>(sp);
+          sw[0] = q[0]; sw[1] = q[1]; sw[2] = q[2];
+        }
+      } else {
+        ld_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, a.codes_len);
+        ld_bytes_clipped<SBYTES>(a.sm, e0 * SMB / 8, sw, a.sm_len);
+      }
+      uint32_t eg[G], ag[G];
+      uint32_t bad = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        uint32_t l0, l1;
+        if constexpr (CB == 4) {
+          const uint32_t cb16 = group_bits<16>(cw, g);
+          l0 = S.lut2[cb16 & 0xFF];
+          l1 = S.lut2[cb16 >> 8];
+        } else {
+          const uint32_t cb12 = group_bits<12>(cw, g);
+          l0 = S.lut2[cb12 & 0x3F];
+          l1 = S.lut2[cb12 >> 6];
+        }
+        eg[g] = __byte_perm(l0, l1, 0x5410);
+        if (check_range) bad |= (((l0 >> 16) & 3) | (((l1 >> 16) & 3) << 2)) << (4 * g);
+        if constexpr (SMB == 8) ag[g] = sw[g];
+        else if constexpr (SMB == 4) ag[g] = unpack_nib4(group_bits<16>(sw, g));
+        else ag[g] = unpack_tri4(group_bits<12>(sw, g));
+      }
+      if (bad) {
+        if (nv < 32) bad &= (1u << nv) - 1u;
+        if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
+      }
+      uint32_t bm;
+      if constexpr (EPV == 32) bm = S.bitmap[s][slot];
+      else bm = (S.bitmap[s][slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
+      if (bm) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int j = 4 * g + b;
+            if ((bm >> j) & 1u) {
+              uint32_t code;
+              if constexpr (CB == 4) code = (cw[j >> 3] >> (4 * (j & 7))) & 0xF;
+              else code = (group_bits<12>(cw, g) >> (3 * b)) & 7;
+              if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+              const uint32_t v = S.vals[s][slot * EPV + j];
+              eg[g] = (eg[g] & ~(0xFFu << (8 * b))) | (v << (8 * b));
+            }
+          }
+        }
+      }
+      uint32_t ow[8];
+#pragma unroll
+      for (int g = 0; g < G; ++g) rebuild_group<FMT>(eg[g], ag[g], ow, g);
+      if (nv == EPV) st256(a.out + e0 * WB, ow);
+      else st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
+    }
+    mbar_arrive(&S.empty[s]);
+  }
+}
+
 __global__ void check_values_kernel(const uint8_t* __restrict__ values, uint64_t m,
                                     const __grid_constant__ sz_params p, sz_decode_status* st) {
   const uint32_t exp_bins = 1u << (p.fmt == SZ_BF16 ? 8 : (p.fmt == SZ_E5M2 ? 5 : 4));
@@ -494,23 +778,47 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   return w;
 }
 
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// Sentinel mode: one CTA per tile, ordinals by block scan + look-back.
+template <int FMT, int CB>
+cudaError_t launch_sentinel(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+  decode_kernel<FMT, CB, 0, kDecodeItems>
+      <<<static_cast<unsigned>(a.num_tiles), kThreads, 0, s>>>(p, a);
+  return cudaGetLastError();
+}
+// Explicit modes: persistent warp-specialised kernel.
 template <int FMT, int CB, int POSB>
-void launch_decode(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
-  decode_kernel<FMT, CB, POSB, kDecodeItems><<<static_cast<unsigned>(a.num_tiles), kThreads, 0, s>>>(p, a);
+cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+  auto kern = decode_persistent<FMT, CB, POSB>;
+  const int smem = static_cast<int>(sizeof(DecSmem<FMT>));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t want = static_cast<uint64_t>(sm_count()) * per_sm;
+  const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
+  kern<<<grid, kDecThreads, smem, s>>>(p, a);
+  return cudaGetLastError();
 }
 template <int FMT, int CB>
-void dec_pos(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+cudaError_t dec_pos(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
   switch (posb) {
-    case 0: launch_decode<FMT, CB, 0>(p, a, s); break;
-    case 1: launch_decode<FMT, CB, 1>(p, a, s); break;
-    case 2: launch_decode<FMT, CB, 2>(p, a, s); break;
-    default: launch_decode<FMT, CB, 4>(p, a, s); break;
+    case 0: return launch_sentinel<FMT, CB>(p, a, s);
+    case 1: return launch_persistent<FMT, CB, 1>(p, a, s);
+    case 2: return launch_persistent<FMT, CB, 2>(p, a, s);
+    default: return launch_persistent<FMT, CB, 4>(p, a, s);
   }
 }
 template <int FMT>
-void dec_cb(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
-  if (p.code_bits == 4) dec_pos<FMT, 4>(posb, p, a, s);
-  else dec_pos<FMT, 3>(posb, p, a, s);
+cudaError_t dec_cb(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
+  return p.code_bits == 4 ? dec_pos<FMT, 4>(posb, p, a, s) : dec_pos<FMT, 3>(posb, p, a, s);
 }
 
 }  // namespace
@@ -586,11 +894,10 @@ int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   a.chunk_shift = (p->chunk_size & (p->chunk_size - 1)) == 0 ? __builtin_ctz(p->chunk_size) : -1;
   const int posb = p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
   switch (p->fmt) {
-    case SZ_BF16: dec_cb<SZ_BF16>(posb, *p, a, s); break;
-    case SZ_E5M2: dec_cb<SZ_E5M2>(posb, *p, a, s); break;
-    default: dec_cb<SZ_E4M3>(posb, *p, a, s); break;
+    case SZ_BF16: e = dec_cb<SZ_BF16>(posb, *p, a, s); break;
+    case SZ_E5M2: e = dec_cb<SZ_E5M2>(posb, *p, a, s); break;
+    default: e = dec_cb<SZ_E4M3>(posb, *p, a, s); break;
   }
-  e = cudaGetLastError();
   return e == cudaSuccess ? SZ_OK : sz_record_cuda(e);
 }
 

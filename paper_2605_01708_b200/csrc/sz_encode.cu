@@ -1,27 +1,41 @@
 // sz_encode.cu — K2: single-pass SplitZip encoder for sm_100a.
 //
 // Replaces codec.py:299-321 (encode) and its byte-identical Quad64 variant
-// codec.py:324-401 (encode_quad).  One CTA = one tile of
-// ITEMS x 256 x EPV elements (EPV = 16 BF16 / 32 FP8 words = one 32-byte
-// vector per "slot"; slot s = item * 256 + thread, element order).
+// codec.py:324-401 (encode_quad).
 //
-//   1. 256-bit streaming loads of the tile (LDG.E.256, L1 no-allocate).
-//   2. Per 4 elements: split fields with byte permutes, look the exponents up
-//      in the marked LUT (shared memory; bit 4 = escape, low bits = code to
-//      store, as in encode_quad's marked table codec.py:340-342), pack the
-//      codes (4-bit nibbles or 3-bit LE stream) and the sign|mantissa plane
-//      (byte plane for BF16, 3/4-bit LE stream for FP8), store both with
-//      vector stores.  Escape flags come out of the same LUT byte.
-//   3. Escape compaction in ascending element order: per-slot popc counts,
-//      block-wide exclusive scan in slot order, decoupled look-back across
-//      tiles (dynamic tile ids => forward progress), then each thread writes
-//      its escapes' (position, raw exponent) records at their global ordinal.
-//   4. Per-chunk escape counts (codec.py:292-295): directly from the block
-//      scan when chunks tile the CTA tile, else by integer atomics into a
-//      zeroed array (deterministic: the sums do not depend on order).
+// Persistent, warp-specialised kernel (two CTAs per SM, 10 warps each):
+//
+//   warp 8  PRODUCER  claims tiles (global atomic counter, so tile ids are
+//                     handed out in order to running CTAs => look-back
+//                     forward progress) and streams each 16 KiB tile of input
+//                     words into a shared-memory ring with a 1-D TMA bulk copy
+//                     (cp.async.bulk -> UBLKCP), completion on an mbarrier.
+//   warps 0-7 DENSE   per 32-byte slot (16 BF16 / 32 FP8 words): split fields
+//                     with byte permutes, exponent -> marked code through the
+//                     shared-memory LUT (bit 4 = escape, as encode_quad's
+//                     marked table codec.py:340-342), pack the 4-bit nibble /
+//                     3-bit LE code plane and the sign|mantissa plane (byte
+//                     plane for BF16, 3/4-bit LE stream for FP8), vector-store
+//                     both, and leave the slot's escape bitmask in smem.
+//   warp 9    SCAN    per tile: popc of the slot masks, warp scan, decoupled
+//                     look-back over the tile-state array for the global
+//                     escape ordinal, per-chunk counts (codec.py:292-295),
+//                     then writes every escape's (position, raw exponent)
+//                     record in ascending element order and frees the stage.
+//
+// The look-back latency is hidden behind the ring: the dense warps keep
+// streaming later tiles while the scan warp waits on predecessors.
 #include "sz_common.cuh"
 
 namespace sz {
+
+constexpr int kEncStages = 4;
+constexpr int kEncItems = 2;                           // slots per dense thread
+constexpr int kEncSlots = kEncItems * kThreads;        // 512 slots per tile
+constexpr int kEncTileBytes = kEncSlots * 32;          // 16 KiB of input words
+constexpr int kEncThreads = kThreads + 64;             // + producer + scan warps
+constexpr int kProducerWarp = kWarps;                  // warp 8
+constexpr int kScanWarp = kWarps + 1;                  // warp 9
 
 struct EncodeArgs {
   const uint8_t* words;
@@ -41,7 +55,18 @@ struct EncodeArgs {
   uint64_t sm_len;
   uint32_t chunk;
   int32_t chunk_shift;   // log2(chunk) when a power of two, else -1
-  int32_t counts_mode;   // 0 none, 1 direct from scan, 2 atomics (pre-zeroed)
+  int32_t counts_mode;   // 0 none, 1 direct from the scan, 2 atomics (pre-zeroed)
+};
+
+struct EncSmem {
+  alignas(128) uint8_t in[kEncStages][kEncTileBytes];
+  uint32_t fmask[kEncStages][kEncSlots];
+  uint32_t pref[kEncSlots + 1];
+  uint64_t meta[kEncStages];
+  uint64_t full[kEncStages];
+  uint64_t computed[kEncStages];
+  uint64_t empty[kEncStages];
+  uint8_t lut[256];
 };
 
 template <int FMT>
@@ -68,188 +93,256 @@ __device__ __forceinline__ uint32_t lut4(const uint8_t* lut, uint32_t e4) {
   return __byte_perm(__byte_perm(m0, m1, 0x0040), __byte_perm(m2, m3, 0x0040), 0x5410);
 }
 
-template <int FMT, int CB, int POSB, int ITEMS>
-__global__ void __launch_bounds__(kThreads)
-    encode_kernel(const __grid_constant__ sz_params p, const EncodeArgs a) {
+template <int FMT>
+__device__ __forceinline__ uint32_t raw_exponent(uint32_t word) {
+  if constexpr (FMT == SZ_BF16) return (word >> 7) & 0xFF;
+  else if constexpr (FMT == SZ_E5M2) return (word >> 2) & 0x1F;
+  else return (word >> 3) & 0x0F;
+}
+
+// Dense transform of one 32-byte slot; returns the slot's escape bitmask.
+template <int FMT, int CB>
+__device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const uint8_t* lut,
+                                                int nv, const EncodeArgs& a, uint64_t e0) {
   constexpr int EPV = kEpv<FMT>;
   constexpr int G = EPV / 4;
-  constexpr int WB = Fmt<FMT>::kWordBytes;
   constexpr int SMB = Fmt<FMT>::kSmBits;
   constexpr int CBYTES = EPV * CB / 8;
   constexpr int SBYTES = EPV * SMB / 8;
   constexpr int CWORDS = (CBYTES + 3) / 4;
   constexpr int SWORDS = (SBYTES + 3) / 4;
-  constexpr int SLOTS = ITEMS * kThreads;
-  constexpr uint64_t TILE = static_cast<uint64_t>(SLOTS) * EPV;
+  uint32_t mk[G], ag[G];
+  uint32_t any = 0;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    uint32_t e4, a4;
+    split_group<FMT>(x, g, e4, a4);
+    uint32_t m4 = lut4(lut, e4);
+    if (nv < EPV) {  // tail slot: zero codes, flags and SM beyond N
+      const int v = min(max(nv - 4 * g, 0), 4);
+      const uint32_t keep = v >= 4 ? 0xFFFFFFFFu : ((1u << (8 * v)) - 1u);
+      m4 &= keep;
+      a4 &= keep;
+    }
+    mk[g] = m4;
+    ag[g] = a4;
+    any |= m4;
+  }
+  uint32_t fm = 0;
+  if (any & 0x10101010u) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) fm |= flags4(mk[g]) << (4 * g);
+  }
+  uint32_t cw[CWORDS], sw[SWORDS];
+  {
+    uint32_t grp[G];
+    if constexpr (CB == 4) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) grp[g] = pack_nib4(mk[g] & 0x0F0F0F0Fu);
+      concat_groups<G, 16>(grp, cw);
+    } else {
+#pragma unroll
+      for (int g = 0; g < G; ++g) grp[g] = pack_tri4(mk[g] & 0x07070707u);
+      concat_groups<G, 12>(grp, cw);
+    }
+  }
+  if constexpr (SMB == 8) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) sw[g] = ag[g];
+  } else {
+    uint32_t grp[G];
+    if constexpr (SMB == 4) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) grp[g] = pack_nib4(ag[g]);
+      concat_groups<G, 16>(grp, sw);
+    } else {
+#pragma unroll
+      for (int g = 0; g < G; ++g) grp[g] = pack_tri4(ag[g]);
+      concat_groups<G, 12>(grp, sw);
+    }
+  }
+  const uint64_t coff = e0 * CB / 8, soff = e0 * SMB / 8;
+  if (nv == EPV) {
+    st_packed<CBYTES>(a.codes + coff, cw);
+    st_packed<SBYTES>(a.sm + soff, sw);
+  } else if (nv > 0) {
+    st_bytes_clipped<CBYTES>(a.codes, coff, cw, a.codes_len);
+    st_bytes_clipped<SBYTES>(a.sm, soff, sw, a.sm_len);
+  }
+  return fm;
+}
 
-  __shared__ uint8_t lut[256];
-  __shared__ BlockScanSmem<ITEMS> scan_sm;
-  __shared__ uint32_t s_prefix[SLOTS + 1];
-  __shared__ unsigned long long s_tile;
-  __shared__ uint64_t s_excl;
+template <int FMT, int CB, int POSB>
+__global__ void __launch_bounds__(kEncThreads, 2)
+    encode_kernel(const __grid_constant__ sz_params p, const EncodeArgs a) {
+  constexpr int EPV = kEpv<FMT>;
+  constexpr int WB = Fmt<FMT>::kWordBytes;
+  constexpr uint64_t TILE = static_cast<uint64_t>(kEncSlots) * EPV;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  EncSmem& S = *reinterpret_cast<EncSmem*>(smem_raw);
 
-  const int tid = threadIdx.x;
-  for (int i = tid; i < 256; i += kThreads) lut[i] = p.enc_lut[i];
-  if (tid == 0) s_tile = atomicAdd(a.tile_counter, 1ull);
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t tile_e0 = tile * TILE;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
-
-  // ---- 1. loads (all items in flight before any compute)
-  uint32_t x[ITEMS][8];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint64_t e0 = tile_e0 + static_cast<uint64_t>(i * kThreads + tid) * EPV;
-    if (e0 + EPV <= n) {
-      ld_stream256(a.words + e0 * WB, x[i]);
-    } else {
-      ld_bytes_clipped<32>(a.words, e0 * WB, x[i], e0 < n ? n * WB : 0);
+  for (int i = tid; i < 256; i += kEncThreads) S.lut[i] = p.enc_lut[i];
+  if (tid == 0) {
+    for (int s = 0; s < kEncStages; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.computed[s], kThreads);
+      mbar_init(&S.empty[s], 1);
     }
-  }
-
-  // ---- 2. dense transform + stores
-  uint32_t fmask[ITEMS];
-  uint32_t cnt[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint64_t e0 = tile_e0 + static_cast<uint64_t>(i * kThreads + tid) * EPV;
-    const bool full = e0 + EPV <= n;
-    const int nv = full ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
-    uint32_t mk[G], ag[G];
-    uint32_t any = 0;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      uint32_t e4, a4;
-      split_group<FMT>(x[i], g, e4, a4);
-      uint32_t m4 = lut4(lut, e4);
-      if (!full) {
-        const int v = min(max(nv - 4 * g, 0), 4);
-        const uint32_t keep = v >= 4 ? 0xFFFFFFFFu : ((1u << (8 * v)) - 1u);
-        m4 &= keep;
-        a4 &= keep;
-      }
-      mk[g] = m4;
-      ag[g] = a4;
-      any |= m4;
-    }
-    uint32_t fm = 0;
-    if (any & 0x10101010u) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) fm |= flags4(mk[g]) << (4 * g);
-    }
-    fmask[i] = fm;
-    cnt[i] = __popc(fm);
-
-    uint32_t cw[CWORDS], sw[SWORDS];
-    {
-      uint32_t grp[G];
-      if constexpr (CB == 4) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) grp[g] = pack_nib4(mk[g] & 0x0F0F0F0Fu);
-        concat_groups<G, 16>(grp, cw);
-      } else {
-#pragma unroll
-        for (int g = 0; g < G; ++g) grp[g] = pack_tri4(mk[g] & 0x07070707u);
-        concat_groups<G, 12>(grp, cw);
-      }
-    }
-    if constexpr (SMB == 8) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) sw[g] = ag[g];
-    } else {
-      uint32_t grp[G];
-      if constexpr (SMB == 4) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) grp[g] = pack_nib4(ag[g]);
-        concat_groups<G, 16>(grp, sw);
-      } else {
-#pragma unroll
-        for (int g = 0; g < G; ++g) grp[g] = pack_tri4(ag[g]);
-        concat_groups<G, 12>(grp, sw);
-      }
-    }
-    const uint64_t coff = e0 * CB / 8, soff = e0 * SMB / 8;
-    if (full) {
-      st_packed<CBYTES>(a.codes + coff, cw);
-      st_packed<SBYTES>(a.sm + soff, sw);
-    } else if (nv > 0) {
-      st_bytes_clipped<CBYTES>(a.codes, coff, cw, a.codes_len);
-      st_bytes_clipped<SBYTES>(a.sm, soff, sw, a.sm_len);
-    }
-  }
-
-  // ---- 3. escape compaction: block scan + decoupled look-back
-  uint32_t excl[ITEMS];
-  const uint32_t total = block_scan<ITEMS>(cnt, excl, scan_sm);
-  if (tid < 32) {
-    const uint64_t ex = lookback_warp(a.states, tile, total);
-    if (tid == 0) {
-      s_excl = ex;
-      if (tile == a.num_tiles - 1) *a.n_escapes = ex + total;
-    }
-  }
-  if (a.counts_mode == 1) {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) s_prefix[i * kThreads + tid + 1] = excl[i] + cnt[i];
-    if (tid == 0) s_prefix[0] = 0;
+    fence_barrier_init();
   }
   __syncthreads();
-  const uint64_t tile_excl = s_excl;
 
-  bool per_escape_atomics = false;
-  if (a.counts_mode == 2) {
-    const uint64_t last = min(tile_e0 + TILE, n) - 1;
-    const uint64_t k0 = tile_e0 / a.chunk, k1 = last / a.chunk;
-    if (k0 == k1) {
-      if (tid == 0 && total) atomicAdd(&a.counts[k0], total);
-    } else {
-      per_escape_atomics = true;
-    }
-  }
-
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    uint32_t fm = fmask[i];
-    if (!fm) continue;
-    const uint64_t e0 = tile_e0 + static_cast<uint64_t>(i * kThreads + tid) * EPV;
-    uint64_t ord = tile_excl + excl[i];
-    while (fm) {
-      const int j = __ffs(fm) - 1;
-      fm &= fm - 1;
-      const uint64_t idx = e0 + j;
-      // Raw exponent: re-read the (L2-resident) word; escapes are rare, so
-      // this is cheaper than holding the exponent bytes in registers.
-      uint32_t ev;
-      if constexpr (FMT == SZ_BF16) ev = (reinterpret_cast<const uint16_t*>(a.words)[idx] >> 7) & 0xFF;
-      else if constexpr (FMT == SZ_E5M2) ev = (a.words[idx] >> 2) & 0x1F;
-      else ev = (a.words[idx] >> 3) & 0x0F;
-      if (ord < a.capacity) {
-        a.values[ord] = static_cast<uint8_t>(ev);
-        if constexpr (POSB == 4) {
-          static_cast<uint32_t*>(a.positions)[ord] = static_cast<uint32_t>(idx);
-        } else if constexpr (POSB == 2 || POSB == 1) {
-          const uint64_t pos = a.chunk_shift >= 0 ? (idx & (a.chunk - 1)) : (idx % a.chunk);
-          if constexpr (POSB == 2)
-            static_cast<uint16_t*>(a.positions)[ord] = static_cast<uint16_t>(pos);
-          else
-            static_cast<uint8_t*>(a.positions)[ord] = static_cast<uint8_t>(pos);
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t s = it % kEncStages, ph = (it / kEncStages) & 1;
+        mbar_wait(&S.empty[s], ph ^ 1);
+        const uint64_t tile = atomicAdd(a.tile_counter, 1ull);
+        if (tile >= a.num_tiles) {
+          S.meta[s] = ~0ull;
+          mbar_arrive(&S.full[s]);
+          break;
+        }
+        S.meta[s] = tile;
+        const uint64_t e0 = tile * TILE;
+        const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
+        const uint32_t bytes = full_slots * 32;
+        if (bytes) {
+          mbar_arrive_tx(&S.full[s], bytes);
+          tma_load_1d(S.in[s], a.words + e0 * WB, bytes, &S.full[s]);
+        } else {
+          mbar_arrive(&S.full[s]);
         }
       }
-      if (per_escape_atomics) atomicAdd(&a.counts[idx / a.chunk], 1u);
-      ++ord;
     }
+    return;
   }
 
-  // ---- 4. per-chunk counts straight from the scan (chunks tile the CTA tile)
-  if (a.counts_mode == 1) {
-    const uint32_t slots_per_chunk = a.chunk / EPV;
-    const uint32_t chunks_here = static_cast<uint32_t>(TILE / a.chunk);
-    const uint64_t k_base = tile_e0 / a.chunk;
-    for (uint32_t k = tid; k < chunks_here; k += kThreads) {
-      if (k_base + k >= a.n_chunks) break;
-      a.counts[k_base + k] = s_prefix[(k + 1) * slots_per_chunk] - s_prefix[k * slots_per_chunk];
+  if (warp < kWarps) {
+    // ------------------------------------------------------------ dense warps
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t s = it % kEncStages, ph = (it / kEncStages) & 1;
+      mbar_wait(&S.full[s], ph);
+      const uint64_t tile = S.meta[s];
+      if (tile == ~0ull) break;
+      const uint64_t tile_e0 = tile * TILE;
+#pragma unroll
+      for (int i = 0; i < kEncItems; ++i) {
+        const int slot = i * kThreads + tid;
+        const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
+        const int nv = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
+        uint32_t x[8];
+        if (nv == EPV) {
+          const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + slot * 32);
+          const uint4 v0 = src[0], v1 = src[1];
+          x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+          x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+        } else {
+          ld_bytes_clipped<32>(a.words, e0 * WB, x, nv > 0 ? n * WB : 0);
+        }
+        S.fmask[s][slot] = encode_slot<FMT, CB>(x, S.lut, nv, a, e0);
+      }
+      mbar_arrive(&S.computed[s]);
     }
+    return;
+  }
+
+  // ---------------------------------------------------------------- scan warp
+  constexpr int SPL = kEncSlots / 32;  // 16 consecutive slots per lane
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t s = it % kEncStages, ph = (it / kEncStages) & 1;
+    mbar_wait(&S.full[s], ph);
+    const uint64_t tile = S.meta[s];
+    if (tile == ~0ull) break;
+    mbar_wait(&S.computed[s], ph);
+    const uint64_t tile_e0 = tile * TILE;
+
+    uint32_t msk[SPL];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      msk[j] = S.fmask[s][lane * SPL + j];
+      cnt += __popc(msk[j]);
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint64_t tile_excl = lookback_warp(a.states, tile, total);
+    if (lane == 0 && tile == a.num_tiles - 1) *a.n_escapes = tile_excl + total;
+
+    if (a.counts_mode == 1) {
+      // chunks tile the CTA tile: count = difference of slot prefixes
+      uint32_t run = incl - cnt;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        run += __popc(msk[j]);
+        S.pref[lane * SPL + j + 1] = run;
+      }
+      if (lane == 0) S.pref[0] = 0;
+      __syncwarp();
+      const uint32_t spc = a.chunk / EPV;
+      const uint32_t chunks_here = static_cast<uint32_t>(TILE / a.chunk);
+      const uint64_t k_base = tile_e0 / a.chunk;
+      for (uint32_t k = lane; k < chunks_here && k_base + k < a.n_chunks; k += 32)
+        a.counts[k_base + k] = S.pref[(k + 1) * spc] - S.pref[k * spc];
+    }
+    bool per_escape_atomics = false;
+    if (a.counts_mode == 2) {
+      const uint64_t last = min(tile_e0 + TILE, n) - 1;
+      const uint64_t k0 = tile_e0 / a.chunk;
+      if (k0 == last / a.chunk) {
+        if (lane == 0 && total) atomicAdd(&a.counts[k0], total);
+      } else {
+        per_escape_atomics = true;
+      }
+    }
+
+    if (total) {
+      uint64_t ord = tile_excl + incl - cnt;
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) {
+        uint32_t m = msk[j];
+        const uint32_t slot = lane * SPL + j;
+        const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
+        const bool in_smem = e0 + EPV <= n;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          const uint64_t idx = e0 + b;
+          uint32_t word;
+          if (in_smem) {
+            const uint8_t* w = S.in[s] + (slot * EPV + b) * WB;
+            word = WB == 2 ? *reinterpret_cast<const uint16_t*>(w) : *w;
+          } else {
+            word = WB == 2 ? reinterpret_cast<const uint16_t*>(a.words)[idx] : a.words[idx];
+          }
+          if (ord < a.capacity) {
+            a.values[ord] = static_cast<uint8_t>(raw_exponent<FMT>(word));
+            if constexpr (POSB == 4) {
+              static_cast<uint32_t*>(a.positions)[ord] = static_cast<uint32_t>(idx);
+            } else if constexpr (POSB == 2 || POSB == 1) {
+              const uint64_t pos =
+                  a.chunk_shift >= 0 ? (idx & (a.chunk - 1)) : (idx % a.chunk);
+              if constexpr (POSB == 2)
+                static_cast<uint16_t*>(a.positions)[ord] = static_cast<uint16_t>(pos);
+              else
+                static_cast<uint8_t*>(a.positions)[ord] = static_cast<uint8_t>(pos);
+            }
+          }
+          if (per_escape_atomics) atomicAdd(&a.counts[idx / a.chunk], 1u);
+          ++ord;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
   }
 }
 
@@ -283,39 +376,46 @@ namespace {
 
 using namespace sz;
 
-constexpr int kEncodeItems = 2;
-
-template <int FMT>
-constexpr uint64_t encode_tile() {
-  return static_cast<uint64_t>(kEncodeItems) * kThreads * kEpv<FMT>;
+uint64_t encode_tile_for(uint32_t fmt) {
+  return static_cast<uint64_t>(kEncSlots) * (fmt == SZ_BF16 ? 16 : 32);
 }
 
-uint64_t encode_tile_for(uint32_t fmt) {
-  return fmt == SZ_BF16 ? encode_tile<SZ_BF16>() : encode_tile<SZ_E5M2>();
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
 }
 
 template <int FMT, int CB, int POSB>
-void launch_encode(const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
-  const unsigned grid = static_cast<unsigned>(a.num_tiles);
-  encode_kernel<FMT, CB, POSB, kEncodeItems><<<grid, kThreads, 0, s>>>(p, a);
+cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
+  auto kern = encode_kernel<FMT, CB, POSB>;
+  const int smem = static_cast<int>(sizeof(EncSmem));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEncThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t want = static_cast<uint64_t>(sm_count()) * per_sm;
+  const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
+  kern<<<grid, kEncThreads, smem, s>>>(p, a);
+  return cudaGetLastError();
 }
 
 template <int FMT, int CB>
-void dispatch_pos(int posb, const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
+cudaError_t dispatch_pos(int posb, const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
   switch (posb) {
-    case 0: launch_encode<FMT, CB, 0>(p, a, s); break;
-    case 1: launch_encode<FMT, CB, 1>(p, a, s); break;
-    case 2: launch_encode<FMT, CB, 2>(p, a, s); break;
-    default: launch_encode<FMT, CB, 4>(p, a, s); break;
+    case 0: return launch_encode<FMT, CB, 0>(p, a, s);
+    case 1: return launch_encode<FMT, CB, 1>(p, a, s);
+    case 2: return launch_encode<FMT, CB, 2>(p, a, s);
+    default: return launch_encode<FMT, CB, 4>(p, a, s);
   }
 }
 
 template <int FMT>
-void dispatch_cb(int posb, const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
-  if (p.code_bits == 4)
-    dispatch_pos<FMT, 4>(posb, p, a, s);
-  else
-    dispatch_pos<FMT, 3>(posb, p, a, s);
+cudaError_t dispatch_cb(int posb, const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
+  return p.code_bits == 4 ? dispatch_pos<FMT, 4>(posb, p, a, s)
+                          : dispatch_pos<FMT, 3>(posb, p, a, s);
 }
 
 }  // namespace
@@ -335,7 +435,8 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
               void* d_ws, size_t ws_bytes, void* stream) {
   if (int rc = sz_check_params(p, 0)) return rc;
   if (n == 0 || !out || !d_words) return SZ_ECONFIG;
-  if ((reinterpret_cast<uintptr_t>(d_words) & 31) || (reinterpret_cast<uintptr_t>(out->d_codes) & 15) ||
+  if ((reinterpret_cast<uintptr_t>(d_words) & 31) ||
+      (reinterpret_cast<uintptr_t>(out->d_codes) & 15) ||
       (reinterpret_cast<uintptr_t>(out->d_sm) & 15))
     return SZ_EALIGN;
   if (ws_bytes < sz_encode_workspace_bytes(n, p)) return SZ_EWORKSPACE;
@@ -378,11 +479,10 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
 
   const int posb = p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
   switch (p->fmt) {
-    case SZ_BF16: dispatch_cb<SZ_BF16>(posb, *p, a, s); break;
-    case SZ_E5M2: dispatch_cb<SZ_E5M2>(posb, *p, a, s); break;
-    default: dispatch_cb<SZ_E4M3>(posb, *p, a, s); break;
+    case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, s); break;
+    case SZ_E5M2: e = dispatch_cb<SZ_E5M2>(posb, *p, a, s); break;
+    default: e = dispatch_cb<SZ_E4M3>(posb, *p, a, s); break;
   }
-  e = cudaGetLastError();
   if (e != cudaSuccess) return sz_record_cuda(e);
   if (exp_bits != 8 && a.capacity) {
     if (!out->d_values_packed) return SZ_ECONFIG;
