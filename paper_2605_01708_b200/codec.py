@@ -386,10 +386,27 @@ def _counts_np(streams) -> np.ndarray | None:
     return None if c is None else to_numpy(c).astype(np.int64)
 
 
+def _check_values_device(values: torch.Tensor, m: int, config: CodecConfig,
+                         codebook: ExponentCodebook) -> list:
+    lib = N.load_library()
+    status = torch.empty(N.STATUS_BYTES, dtype=torch.uint8, device=values.device)
+    N.check(lib.sz_check_values(N.ptr(values), m, _config_params(config, codebook),
+                                N.ptr(status), N.stream_handle()), "check_values")
+    return _status_view(status.cpu().numpy())[1]
+
+
 def _raise_from_status(raw: np.ndarray, streams: EncodedStreams, config: CodecConfig,
-                       codebook: ExponentCodebook, codes_dev: torch.Tensor) -> None:
+                       codebook: ExponentCodebook, values_dev: torch.Tensor | None) -> None:
     st, first = _status_view(raw)
     flags = st.flags
+    if (config.chunked and flags & (1 << N.DEC_COUNTS_TOTAL) and values_dev is not None
+            and streams.n_escapes):
+        # The fused kernel checks escape values only for ordinals its tiles
+        # visit; with inconsistent counts some are never visited, and the
+        # reference checks values first (codec.py:446-457) — complete them.
+        full = _check_values_device(values_dev, int(streams.n_escapes), config, codebook)
+        first[N.DEC_VALUE_DOMAIN] = full[N.DEC_VALUE_DOMAIN]
+        first[N.DEC_VALUE_IN_BOOK] = full[N.DEC_VALUE_IN_BOOK]
     if first[N.DEC_CODE_PAD] is not None:
         raise CorruptionError("nonzero padding bits in code stream")
     if first[N.DEC_SM_PAD] is not None:
@@ -495,7 +512,7 @@ def decode(streams: EncodedStreams, config: CodecConfig,
     N.check(lib.sz_decode(src, params, N.ptr(out), N.ptr(status), N.ptr(ws), ws.numel(),
                           N.stream_handle()), "decode")
     raw = status.cpu().numpy()
-    _raise_from_status(raw, streams, config, codebook, codes)
+    _raise_from_status(raw, streams, config, codebook, values)
     if streams.on_device or is_device(streams.packed_codes):
         return RawTensorStream(fmt, out)
     return RawTensorStream(fmt, out.cpu().numpy())

@@ -221,6 +221,51 @@ constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
 constexpr uint64_t kValueMask = (1ull << 62) - 1;
 
+// Wide look-back: ALL lanes of one warp; every lane reads E predecessor
+// states per round (32*E per L2 round trip), so the look-back over W
+// concurrently-running tiles costs ceil(W / 32E) round trips instead of W/32.
+// The caller's own aggregate must already be published (or tile == 0).
+// Returns the exclusive prefix of `tile` in every lane; does not publish.
+template <int E>
+__device__ __forceinline__ uint64_t lookback_wide(const uint64_t* states, uint64_t tile) {
+  const int lane = threadIdx.x & 31;
+  uint64_t excl = 0;
+  int64_t pred = static_cast<int64_t>(tile) - 1;
+  while (pred >= 0) {
+    uint64_t st[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int64_t idx = pred - (lane * E + j);
+      st[j] = idx >= 0 ? ld_relaxed(&states[idx]) : kFlagPrefix;
+    }
+    int first = 32 * E;  // distance of the nearest inclusive prefix seen by this lane
+#pragma unroll
+    for (int j = E - 1; j >= 0; --j)
+      if ((st[j] >> 62) == 2) first = lane * E + j;
+    first = __reduce_min_sync(0xffffffffu, first);
+    bool missing = false;
+    uint64_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int d = lane * E + j;
+      if (d <= first) {
+        missing |= (st[j] >> 62) == 0;
+        sum += st[j] & kValueMask;
+      }
+    }
+    if (__any_sync(0xffffffffu, missing)) {
+      __nanosleep(64);
+      continue;
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+    excl += sum;
+    if (first < 32 * E) break;
+    pred -= 32 * E;
+  }
+  return excl;
+}
+
 // Called by ALL lanes of one warp.  Publishes `agg` for `tile`, walks back to
 // the nearest inclusive prefix, publishes this tile's inclusive prefix and
 // returns the exclusive prefix (in every lane).
@@ -232,26 +277,8 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* states, uint64_t til
     return 0;
   }
   if (lane == 0) st_relaxed(&states[tile], kFlagAgg | agg);
-  uint64_t excl = 0;
-  int64_t pred = static_cast<int64_t>(tile) - 1;
-  while (true) {
-    const int64_t idx = pred - lane;
-    uint64_t s = idx >= 0 ? ld_relaxed(&states[idx]) : kFlagPrefix;
-    uint32_t flag = static_cast<uint32_t>(s >> 62);
-    if (__any_sync(0xffffffffu, flag == 0)) {
-      __nanosleep(32);
-      continue;
-    }
-    const uint32_t pmask = __ballot_sync(0xffffffffu, flag == 2);
-    uint64_t v = s & kValueMask;
-    int stop = pmask ? __ffs(pmask) - 1 : 31;
-    if (lane > stop) v = 0;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    excl += v;
-    if (pmask) break;
-    pred -= 32;
-  }
+  __syncwarp();
+  const uint64_t excl = lookback_wide<8>(states, tile);
   if (lane == 0) st_relaxed(&states[tile], kFlagPrefix | (excl + agg));
   return excl;
 }

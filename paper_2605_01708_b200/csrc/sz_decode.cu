@@ -446,27 +446,27 @@ __global__ void __launch_bounds__(kThreads)
 // (bitmap + raw values in smem) and runs every per-escape check; warps 0-7
 // decode slots from smem and write 256-bit stores.  No CTA-wide barriers in
 // steady state — only mbarrier hand-offs.
-constexpr int kDecStages = 4;
 constexpr int kDecItems = 2;
 constexpr int kDecSlots = kDecItems * kThreads;        // 512 slots per tile
-constexpr int kDecThreads = kThreads + 64;
-constexpr int kDecPlaneBytes = kDecSlots * 16;         // max bytes of one plane per tile
-constexpr int kDecOffStage = 1024;
+constexpr int kDecHelpers = 3;                          // escape-staging warps
+constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
+constexpr int kDecOffStage = 256;                       // staged chunk offsets per helper
 
 template <int FMT>
 struct DecSmem {
+  static constexpr int STAGES = FMT == SZ_BF16 ? 4 : 3;
   static constexpr int EPV = kEpv<FMT>;
   static constexpr int TILE = kDecSlots * EPV;
-  alignas(128) uint8_t codes[kDecStages][kDecPlaneBytes];
-  alignas(128) uint8_t sm[kDecStages][kDecPlaneBytes];
-  alignas(16) uint8_t vals[kDecStages][TILE];
-  uint32_t bitmap[kDecStages][TILE / 32];
-  uint64_t off[kDecOffStage + 1];
+  alignas(128) uint8_t codes[STAGES][TILE / 2];              // <= 4-bit codes
+  alignas(128) uint8_t sm[STAGES][TILE * Fmt<FMT>::kSmBits / 8];
+  alignas(16) uint8_t vals[STAGES][TILE];
+  uint32_t bitmap[STAGES][TILE / 32];
+  uint64_t off[kDecHelpers][kDecOffStage + 1];
   uint32_t lut2[256];
-  uint64_t meta[kDecStages];
-  uint64_t full[kDecStages];
-  uint64_t staged[kDecStages];
-  uint64_t empty[kDecStages];
+  uint64_t meta[STAGES];
+  uint64_t full[STAGES];
+  uint64_t staged[STAGES];
+  uint64_t empty[STAGES];
 };
 
 template <int FMT, int CB, int POSB>
@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   constexpr int LUT2 = CB == 4 ? 256 : 64;
   constexpr uint32_t kCodeMask = (1u << CB) - 1;
   using Smem = DecSmem<FMT>;
+  constexpr int kStages = Smem::STAGES;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
 
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     S.lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
   if (tid == 0) {
-    for (int s = 0; s < kDecStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.staged[s], 1);
       mbar_init(&S.empty[s], kThreads);
@@ -509,12 +510,17 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       for (uint32_t it = 0;; ++it) {
-        const uint32_t s = it % kDecStages, ph = (it / kDecStages) & 1;
+        const uint32_t s = it % kStages, ph = (it / kStages) & 1;
         mbar_wait(&S.empty[s], ph ^ 1);
         const uint64_t tile = atomicAdd(a.tile_counter, 1ull);
         if (tile >= a.num_tiles) {
-          S.meta[s] = ~0ull;
-          mbar_arrive(&S.full[s]);
+          // end markers: this iteration (decode warps) and one per helper
+          for (uint32_t k = 0; k < kDecHelpers; ++k) {
+            const uint32_t sk = (it + k) % kStages, pk = ((it + k) / kStages) & 1;
+            if (k) mbar_wait(&S.empty[sk], pk ^ 1);
+            S.meta[sk] = ~0ull;
+            mbar_arrive(&S.full[sk]);
+          }
           break;
         }
         S.meta[s] = tile;
@@ -530,33 +536,35 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     return;
   }
 
-  if (warp == kWarps + 1) {
-    // ------------------------------------------------------------ escape stager
+  if (warp > kWarps) {
+    // ------------------------------------------------------------ escape stagers
+    // kDecHelpers warps, helper h owns iterations it == h (mod kDecHelpers), so
+    // the dependent global loads of several tiles are in flight at once.
     const uint32_t exp_bins = 1u << Fmt<FMT>::kExpBits;
-    for (uint32_t it = 0;; ++it) {
-      const uint32_t s = it % kDecStages, ph = (it / kDecStages) & 1;
+    const int h = warp - kWarps - 1;
+    uint64_t* soff = S.off[h];
+    for (uint32_t it = h;; it += kDecHelpers) {
+      const uint32_t s = it % kStages, ph = (it / kStages) & 1;
       mbar_wait(&S.full[s], ph);
       const uint64_t tile = S.meta[s];
       if (tile == ~0ull) break;
       const uint64_t s0 = tile * TILE, s1 = min(s0 + TILE, n);
 #pragma unroll
       for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
-      // per-ordinal checks independent of the counts, spread evenly over tiles
-      {
+      if constexpr (ABS) {
+        // abs32: per-ordinal checks spread evenly over tiles (the staging
+        // below only visits ordinals whose positions land in some tile)
         const uint64_t q = (m + a.num_tiles - 1) / a.num_tiles;
         const uint64_t o0 = tile * q, o1 = min(o0 + q, m);
+        const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
         for (uint64_t o = o0 + lane; o < o1; o += 32) {
           const uint32_t v = a.values[o];
           if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
           else if (!(p.enc_lut[v] & 0x10))
             record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-          if constexpr (ABS) {
-            const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
-            const uint32_t pv = pos[o];
-            if (pv >= n) record_first(&a.status->first_inv[SZ_DEC_ABS_PAST_END], o);
-            if (o > 0 && pv <= pos[o - 1])
-              record_first(&a.status->first_inv[SZ_DEC_ABS_NOT_INC], o);
-          }
+          const uint32_t pv = pos[o];
+          if (pv >= n) record_first(&a.status->first_inv[SZ_DEC_ABS_PAST_END], o);
+          if (o > 0 && pv <= pos[o - 1]) record_first(&a.status->first_inv[SZ_DEC_ABS_NOT_INC], o);
         }
       }
       if (tile == a.num_tiles - 1 && lane == 0) {
@@ -587,17 +595,32 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         const uint64_t nk = kb - ka + 2;
         const bool staged = nk <= kDecOffStage + 1;
         if (staged)
-          for (uint64_t i = lane; i < nk; i += 32) S.off[i] = a.offsets[ka + i];
+          for (uint64_t i = lane; i < nk; i += 32) soff[i] = a.offsets[ka + i];
         __syncwarp();
-        const uint64_t* off = staged ? S.off : a.offsets + ka;
+        const uint64_t* off = staged ? soff : a.offsets + ka;
         const uint64_t o_lo = min(off[0], m), o_hi = min(off[nk - 1], m);
-        for (uint64_t o = o_lo + lane; o < o_hi; o += 32) {
+        // 32 consecutive ordinals per round: coalesced position/value loads,
+        // the predecessor's position comes from the neighbouring lane.
+        uint64_t carry = 0;  // position of ordinal base-1 (previous round's lane 31)
+        for (uint64_t base = o_lo; base < o_hi; base += 32) {
+          const uint64_t o = base + lane;
+          const bool live = o < o_hi;
+          const uint64_t pv = live ? load_pos<POSB>(a.positions, o) : 0;
+          const uint32_t v = live ? a.values[o] : 0;
+          uint64_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
+          if (lane == 0) prev = carry;
+          carry = __shfl_sync(0xffffffffu, pv, 31);
+          if (!live) continue;
+          // per-ordinal value checks (codec.py:451-457); complete coverage when
+          // sum(counts) != M is restored on the host (sz_check_values)
+          if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+          else if (!(p.enc_lut[v] & 0x10))
+            record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
           uint64_t lo = 0, hi = nk - 1;
           while (hi - lo > 1) {
             const uint64_t mid = (lo + hi) >> 1;
             if (off[mid] <= o) lo = mid; else hi = mid;
           }
-          const uint64_t pv = load_pos<POSB>(a.positions, o);
           if (pv >= a.chunk) {
             record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
             continue;
@@ -607,12 +630,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
             continue;
           }
-          if (o > off[lo] && load_pos<POSB>(a.positions, o - 1) >= pv)
-            record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+          if (o > off[lo] && prev >= pv) record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
           if (idx >= s0 && idx < s1) {
             const uint32_t rel = static_cast<uint32_t>(idx - s0);
             atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
-            S.vals[s][rel] = a.values[o];
+            S.vals[s][rel] = static_cast<uint8_t>(v);
           }
         }
       }
@@ -625,7 +647,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   // ------------------------------------------------------------ decode warps
   const bool check_range = p.n_entries < (1u << CB);
   for (uint32_t it = 0;; ++it) {
-    const uint32_t s = it % kDecStages, ph = (it / kDecStages) & 1;
+    const uint32_t s = it % kStages, ph = (it / kStages) & 1;
     mbar_wait(&S.full[s], ph);
     const uint64_t tile = S.meta[s];
     if (tile == ~0ull) break;

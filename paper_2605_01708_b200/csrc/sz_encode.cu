@@ -1,41 +1,52 @@
-// sz_encode.cu — K2: single-pass SplitZip encoder for sm_100a.
+// sz_encode.cu — K2: SplitZip encoder for sm_100a.
 //
 // Replaces codec.py:299-321 (encode) and its byte-identical Quad64 variant
-// codec.py:324-401 (encode_quad).
+// codec.py:324-401 (encode_quad).  Two kernels on one stream:
 //
-// Persistent, warp-specialised kernel (two CTAs per SM, 10 warps each):
-//
-//   warp 8  PRODUCER  claims tiles (global atomic counter, so tile ids are
-//                     handed out in order to running CTAs => look-back
-//                     forward progress) and streams each 16 KiB tile of input
-//                     words into a shared-memory ring with a 1-D TMA bulk copy
-//                     (cp.async.bulk -> UBLKCP), completion on an mbarrier.
-//   warps 0-7 DENSE   per 32-byte slot (16 BF16 / 32 FP8 words): split fields
-//                     with byte permutes, exponent -> marked code through the
-//                     shared-memory LUT (bit 4 = escape, as encode_quad's
-//                     marked table codec.py:340-342), pack the 4-bit nibble /
-//                     3-bit LE code plane and the sign|mantissa plane (byte
-//                     plane for BF16, 3/4-bit LE stream for FP8), vector-store
-//                     both, and leave the slot's escape bitmask in smem.
-//   warp 9    SCAN    per tile: popc of the slot masks, warp scan, decoupled
-//                     look-back over the tile-state array for the global
-//                     escape ordinal, per-chunk counts (codec.py:292-295),
-//                     then writes every escape's (position, raw exponent)
-//                     record in ascending element order and frees the stage.
-//
-// The look-back latency is hidden behind the ring: the dense warps keep
-// streaming later tiles while the scan warp waits on predecessors.
+// K2a  encode_tiles — persistent, warp-specialised, one CTA per SM (20 warps):
+//   warp 16    PRODUCER claims 32 KiB tiles of input words (global counter)
+//                       and streams them into a 4-deep shared-memory ring with
+//                       1-D TMA bulk copies (cp.async.bulk -> UBLKCP),
+//                       completion counted on an mbarrier.
+//   warps 0-15 DENSE    per 32-byte slot (16 BF16 / 32 FP8 words): split the
+//                       fields with byte permutes, map exponents through the
+//                       shared-memory marked LUT (bit 4 = escape, encode_quad's
+//                       table codec.py:340-342), pack the 4-bit nibble / 3-bit
+//                       code plane and the sign|mantissa plane (byte plane /
+//                       3-4 bit LE stream), vector-store both; leave the slot's
+//                       escape bitmask (ballot-style) and compact
+//                       (element, raw exponent) records in shared memory.
+//   warps 17-19 WRITER  per tile: popc of the slot masks + warp scan = the
+//                       tile-local escape order, per-chunk counts
+//                       (codec.py:292-295), escape records written in
+//                       ascending element order into the tile's scratch slot.
+//   No CTA ever waits for another, so the stream runs at HBM speed.
+// K2b  escape_gather — decoupled look-back prefix over the per-tile escape
+//   counts (a few hundred KB), then coalesced moves of every tile's records
+//   to their global ordinals in escape_positions / escape_values
+//   (codec.py:281-296); tiles whose escapes overflowed the scratch slot are
+//   re-derived from the input in element order.
+#include <cstdio>
+#include <cstdlib>
+
 #include "sz_common.cuh"
 
 namespace sz {
 
-constexpr int kEncStages = 4;
-constexpr int kEncItems = 2;                           // slots per dense thread
-constexpr int kEncSlots = kEncItems * kThreads;        // 512 slots per tile
-constexpr int kEncTileBytes = kEncSlots * 32;          // 16 KiB of input words
-constexpr int kEncThreads = kThreads + 64;             // + producer + scan warps
-constexpr int kProducerWarp = kWarps;                  // warp 8
-constexpr int kScanWarp = kWarps + 1;                  // warp 9
+constexpr int kEncDenseWarps = 16;
+constexpr int kEncDense = kEncDenseWarps * 32;          // 512 dense threads
+constexpr int kEncItems = 2;                            // slots per dense thread
+constexpr int kEncSlots = kEncItems * kEncDense;         // 1024 slots per tile
+constexpr int kEncTileBytes = kEncSlots * 32;           // 32 KiB of input words
+constexpr int kEncInStages = 4;
+constexpr int kEncScanSlots = 8;
+constexpr int kEscCap = 1024;                           // escape records per tile slot
+// 16 + 1 + 3 = 20 warps: a multiple of 4 so the register file splits evenly
+// (96 registers per thread at one CTA per SM).
+constexpr int kWriterWarps = 3;
+constexpr int kEncThreads = kEncDense + 32 * (1 + kWriterWarps);
+constexpr int kProducerWarp = kEncDenseWarps;           // warp 16
+constexpr int kWriterWarp0 = kEncDenseWarps + 1;        // warps 17..19
 
 struct EncodeArgs {
   const uint8_t* words;
@@ -43,12 +54,6 @@ struct EncodeArgs {
   uint8_t* codes;
   uint8_t* sm;
   uint32_t* counts;
-  void* positions;
-  uint8_t* values;
-  uint64_t* n_escapes;
-  uint64_t capacity;
-  uint64_t* states;
-  unsigned long long* tile_counter;
   uint64_t num_tiles;
   uint64_t n_chunks;
   uint64_t codes_len;
@@ -56,16 +61,26 @@ struct EncodeArgs {
   uint32_t chunk;
   int32_t chunk_shift;   // log2(chunk) when a power of two, else -1
   int32_t counts_mode;   // 0 none, 1 direct from the scan, 2 atomics (pre-zeroed)
+  unsigned long long* tile_counter;
+  uint32_t* tile_esc;    // per-tile escape count
+  uint8_t* scr_pos;      // kEscCap positions per tile (POSB bytes each)
+  uint8_t* scr_val;      // kEscCap raw exponents per tile
+  unsigned long long* dbg;  // optional per-role cycle counters (SZ_DEBUG_TIMERS)
 };
 
 struct EncSmem {
-  alignas(128) uint8_t in[kEncStages][kEncTileBytes];
-  uint32_t fmask[kEncStages][kEncSlots];
-  uint32_t pref[kEncSlots + 1];
-  uint64_t meta[kEncStages];
-  uint64_t full[kEncStages];
-  uint64_t computed[kEncStages];
-  uint64_t empty[kEncStages];
+  alignas(128) uint8_t in[kEncInStages][kEncTileBytes];
+  uint32_t fmask[kEncScanSlots][kEncSlots];
+  // escape records (tile-local element index | raw exponent << 16), in
+  // arbitrary order; the writer warp derives each one's rank from fmask
+  uint32_t esc_rec[kEncScanSlots][kEscCap];
+  uint32_t esc_n[kEncScanSlots];
+  uint16_t slot_pref[kWriterWarps][kEncSlots];  // per-slot exclusive escape prefix
+  uint64_t meta[kEncScanSlots];      // tile id (~0 = end of work)
+  uint64_t full[kEncInStages];       // producer -> dense (TMA bytes)
+  uint64_t in_empty[kEncInStages];   // dense -> producer
+  uint64_t computed[kEncScanSlots];  // dense -> writer
+  uint64_t scan_empty[kEncScanSlots];// writer -> producer
   uint8_t lut[256];
 };
 
@@ -172,12 +187,26 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
   return fm;
 }
 
+// Position of element `idx` in the escape-position stream (codec.py:289-295).
+template <int POSB>
+__device__ __forceinline__ void put_position(uint8_t* base, uint64_t i, uint64_t idx,
+                                             uint32_t chunk, int32_t chunk_shift) {
+  if constexpr (POSB == 4) {
+    reinterpret_cast<uint32_t*>(base)[i] = static_cast<uint32_t>(idx);
+  } else if constexpr (POSB == 2 || POSB == 1) {
+    const uint64_t pos = chunk_shift >= 0 ? (idx & (chunk - 1)) : (idx % chunk);
+    if constexpr (POSB == 2) reinterpret_cast<uint16_t*>(base)[i] = static_cast<uint16_t>(pos);
+    else base[i] = static_cast<uint8_t>(pos);
+  }
+}
+
 template <int FMT, int CB, int POSB>
-__global__ void __launch_bounds__(kEncThreads, 2)
-    encode_kernel(const __grid_constant__ sz_params p, const EncodeArgs a) {
+__global__ void __launch_bounds__(kEncThreads, 1)
+    encode_tiles(const __grid_constant__ sz_params p, const EncodeArgs a) {
   constexpr int EPV = kEpv<FMT>;
   constexpr int WB = Fmt<FMT>::kWordBytes;
   constexpr uint64_t TILE = static_cast<uint64_t>(kEncSlots) * EPV;
+  constexpr int PB = POSB == 0 ? 1 : POSB;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   EncSmem& S = *reinterpret_cast<EncSmem*>(smem_raw);
 
@@ -185,10 +214,14 @@ __global__ void __launch_bounds__(kEncThreads, 2)
   const uint64_t n = a.n;
   for (int i = tid; i < 256; i += kEncThreads) S.lut[i] = p.enc_lut[i];
   if (tid == 0) {
-    for (int s = 0; s < kEncStages; ++s) {
+    for (int s = 0; s < kEncInStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.computed[s], kThreads);
-      mbar_init(&S.empty[s], 1);
+      mbar_init(&S.in_empty[s], kEncDense);
+    }
+    for (int q = 0; q < kEncScanSlots; ++q) {
+      mbar_init(&S.computed[q], kEncDense);
+      mbar_init(&S.scan_empty[q], 1);
+      S.esc_n[q] = 0;
     }
     fence_barrier_init();
   }
@@ -197,16 +230,30 @@ __global__ void __launch_bounds__(kEncThreads, 2)
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
+      long long t_in = 0, t_scan = 0;
       for (uint32_t it = 0;; ++it) {
-        const uint32_t s = it % kEncStages, ph = (it / kEncStages) & 1;
-        mbar_wait(&S.empty[s], ph ^ 1);
+        const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
+        const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
+        const long long c0 = clock64();
+        mbar_wait(&S.in_empty[s], sph ^ 1);
+        const long long c1 = clock64();
+        mbar_wait(&S.scan_empty[q], qph ^ 1);
+        t_in += c1 - c0;
+        t_scan += clock64() - c1;
         const uint64_t tile = atomicAdd(a.tile_counter, 1ull);
         if (tile >= a.num_tiles) {
-          S.meta[s] = ~0ull;
+          // end markers in this slot and the next kWriterWarps-1 (one per
+          // writer residue class); the dense warps relay them (computed)
+          S.meta[q] = ~0ull;
+          for (uint32_t k = 1; k < kWriterWarps; ++k) {
+            const uint32_t qk = (it + k) % kEncScanSlots, pk = ((it + k) / kEncScanSlots) & 1;
+            mbar_wait(&S.scan_empty[qk], pk ^ 1);
+            S.meta[qk] = ~0ull;
+          }
           mbar_arrive(&S.full[s]);
           break;
         }
-        S.meta[s] = tile;
+        S.meta[q] = tile;
         const uint64_t e0 = tile * TILE;
         const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
         const uint32_t bytes = full_slots * 32;
@@ -217,55 +264,101 @@ __global__ void __launch_bounds__(kEncThreads, 2)
           mbar_arrive(&S.full[s]);
         }
       }
+      if (a.dbg) {
+        atomicAdd(&a.dbg[6], static_cast<unsigned long long>(t_in));
+        atomicAdd(&a.dbg[7], static_cast<unsigned long long>(t_scan));
+      }
     }
     return;
   }
 
-  if (warp < kWarps) {
+  if (warp < kEncDenseWarps) {
     // ------------------------------------------------------------ dense warps
+    long long t_wait = 0, t_work = 0;
     for (uint32_t it = 0;; ++it) {
-      const uint32_t s = it % kEncStages, ph = (it / kEncStages) & 1;
-      mbar_wait(&S.full[s], ph);
-      const uint64_t tile = S.meta[s];
-      if (tile == ~0ull) break;
+      const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
+      const uint32_t q = it % kEncScanSlots;
+      const long long c0 = clock64();
+      mbar_wait(&S.full[s], sph);
+      const long long c1 = clock64();
+      t_wait += c1 - c0;
+      const uint64_t tile = S.meta[q];
+      if (tile == ~0ull) {
+        for (uint32_t k = 0; k < kWriterWarps; ++k)
+          mbar_arrive(&S.computed[(it + k) % kEncScanSlots]);
+        break;
+      }
       const uint64_t tile_e0 = tile * TILE;
+      uint32_t x[kEncItems][8];
+      int nv[kEncItems];
 #pragma unroll
       for (int i = 0; i < kEncItems; ++i) {
-        const int slot = i * kThreads + tid;
+        const int slot = i * kEncDense + tid;
         const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
-        const int nv = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
-        uint32_t x[8];
-        if (nv == EPV) {
+        nv[i] = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
+        if (nv[i] == EPV) {
           const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + slot * 32);
           const uint4 v0 = src[0], v1 = src[1];
-          x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
-          x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+          x[i][0] = v0.x; x[i][1] = v0.y; x[i][2] = v0.z; x[i][3] = v0.w;
+          x[i][4] = v1.x; x[i][5] = v1.y; x[i][6] = v1.z; x[i][7] = v1.w;
         } else {
-          ld_bytes_clipped<32>(a.words, e0 * WB, x, nv > 0 ? n * WB : 0);
+          ld_bytes_clipped<32>(a.words, e0 * WB, x[i], nv[i] > 0 ? n * WB : 0);
         }
-        S.fmask[s][slot] = encode_slot<FMT, CB>(x, S.lut, nv, a, e0);
       }
-      mbar_arrive(&S.computed[s]);
+      mbar_arrive(&S.in_empty[s]);  // input stage free: the producer may refill it
+#pragma unroll
+      for (int i = 0; i < kEncItems; ++i) {
+        const int slot = i * kEncDense + tid;
+        const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
+        const uint32_t fm = encode_slot<FMT, CB>(x[i], S.lut, nv[i], a, e0);
+        S.fmask[q][slot] = fm;
+        if (fm) {  // rare: append (element, raw exponent) records for the writer
+          uint32_t r = atomicAdd(&S.esc_n[q], static_cast<uint32_t>(__popc(fm)));
+#pragma unroll
+          for (int j = 0; j < EPV; ++j) {
+            if ((fm >> j) & 1u) {
+              uint32_t word;
+              if constexpr (WB == 2) word = (x[i][j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+              else word = (x[i][j >> 2] >> (8 * (j & 3))) & 0xFFu;
+              if (r < kEscCap)
+                S.esc_rec[q][r] = static_cast<uint32_t>(slot * EPV + j) |
+                                  (raw_exponent<FMT>(word) << 16);
+              ++r;
+            }
+          }
+        }
+      }
+      mbar_arrive(&S.computed[q]);
+      t_work += clock64() - c1;
+    }
+    if (a.dbg && lane == 0) {
+      atomicAdd(&a.dbg[0], static_cast<unsigned long long>(t_wait));
+      atomicAdd(&a.dbg[1], static_cast<unsigned long long>(t_work));
     }
     return;
   }
 
-  // ---------------------------------------------------------------- scan warp
-  constexpr int SPL = kEncSlots / 32;  // 16 consecutive slots per lane
-  for (uint32_t it = 0;; ++it) {
-    const uint32_t s = it % kEncStages, ph = (it / kEncStages) & 1;
-    mbar_wait(&S.full[s], ph);
-    const uint64_t tile = S.meta[s];
+  // ---------------------------------------------------------------- writer warps
+  constexpr int SPL = kEncSlots / 32;  // 32 consecutive slots per lane
+  const int ww = warp - kWriterWarp0;  // owns iterations it == ww (mod kWriterWarps)
+  uint16_t* sp = S.slot_pref[ww];
+  long long t_wait = 0, t_work = 0;
+  for (uint32_t it = ww;; it += kWriterWarps) {
+    const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
+    const long long c0 = clock64();
+    mbar_wait(&S.computed[q], qph);
+    const long long c1 = clock64();
+    t_wait += c1 - c0;
+    const uint64_t tile = S.meta[q];
     if (tile == ~0ull) break;
-    mbar_wait(&S.computed[s], ph);
     const uint64_t tile_e0 = tile * TILE;
 
-    uint32_t msk[SPL];
+    const uint32_t* fm = &S.fmask[q][lane * SPL];
     uint32_t cnt = 0;
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) {
-      msk[j] = S.fmask[s][lane * SPL + j];
-      cnt += __popc(msk[j]);
+    for (int j = 0; j < SPL; j += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(fm + j);
+      cnt += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
     }
     uint32_t incl = cnt;
 #pragma unroll
@@ -273,76 +366,179 @@ __global__ void __launch_bounds__(kEncThreads, 2)
       const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += o;
     }
+    const uint32_t excl_lane = incl - cnt;
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint64_t tile_excl = lookback_warp(a.states, tile, total);
-    if (lane == 0 && tile == a.num_tiles - 1) *a.n_escapes = tile_excl + total;
+    if (lane == 0) a.tile_esc[tile] = total;
 
     if (a.counts_mode == 1) {
-      // chunks tile the CTA tile: count = difference of slot prefixes
-      uint32_t run = incl - cnt;
-#pragma unroll
-      for (int j = 0; j < SPL; ++j) {
-        run += __popc(msk[j]);
-        S.pref[lane * SPL + j + 1] = run;
-      }
-      if (lane == 0) S.pref[0] = 0;
-      __syncwarp();
-      const uint32_t spc = a.chunk / EPV;
-      const uint32_t chunks_here = static_cast<uint32_t>(TILE / a.chunk);
+      // chunks tile the CTA tile (power-of-two chunk): count straight from the
+      // lane scan
+      const uint32_t spc = a.chunk / EPV;                 // slots per chunk
       const uint64_t k_base = tile_e0 / a.chunk;
-      for (uint32_t k = lane; k < chunks_here && k_base + k < a.n_chunks; k += 32)
-        a.counts[k_base + k] = S.pref[(k + 1) * spc] - S.pref[k * spc];
-    }
-    bool per_escape_atomics = false;
-    if (a.counts_mode == 2) {
-      const uint64_t last = min(tile_e0 + TILE, n) - 1;
-      const uint64_t k0 = tile_e0 / a.chunk;
-      if (k0 == last / a.chunk) {
-        if (lane == 0 && total) atomicAdd(&a.counts[k0], total);
+      if (spc >= SPL) {
+        const uint32_t L = spc / SPL;                     // lanes per chunk
+        const uint32_t first = lane & ~(L - 1);
+        const uint32_t start_excl = __shfl_sync(0xffffffffu, excl_lane, first);
+        const uint64_t k = k_base + lane / L;
+        if ((lane & (L - 1)) == L - 1 && k < a.n_chunks) a.counts[k] = incl - start_excl;
       } else {
-        per_escape_atomics = true;
-      }
-    }
-
-    if (total) {
-      uint64_t ord = tile_excl + incl - cnt;
-#pragma unroll
-      for (int j = 0; j < SPL; ++j) {
-        uint32_t m = msk[j];
-        const uint32_t slot = lane * SPL + j;
-        const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
-        const bool in_smem = e0 + EPV <= n;
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          const uint64_t idx = e0 + b;
-          uint32_t word;
-          if (in_smem) {
-            const uint8_t* w = S.in[s] + (slot * EPV + b) * WB;
-            word = WB == 2 ? *reinterpret_cast<const uint16_t*>(w) : *w;
-          } else {
-            word = WB == 2 ? reinterpret_cast<const uint16_t*>(a.words)[idx] : a.words[idx];
-          }
-          if (ord < a.capacity) {
-            a.values[ord] = static_cast<uint8_t>(raw_exponent<FMT>(word));
-            if constexpr (POSB == 4) {
-              static_cast<uint32_t*>(a.positions)[ord] = static_cast<uint32_t>(idx);
-            } else if constexpr (POSB == 2 || POSB == 1) {
-              const uint64_t pos =
-                  a.chunk_shift >= 0 ? (idx & (a.chunk - 1)) : (idx % a.chunk);
-              if constexpr (POSB == 2)
-                static_cast<uint16_t*>(a.positions)[ord] = static_cast<uint16_t>(pos);
-              else
-                static_cast<uint8_t*>(a.positions)[ord] = static_cast<uint8_t>(pos);
-            }
-          }
-          if (per_escape_atomics) atomicAdd(&a.counts[idx / a.chunk], 1u);
-          ++ord;
+        const uint32_t per_lane = SPL / spc;
+        for (uint32_t c = 0; c < per_lane; ++c) {
+          uint32_t sum = 0;
+          for (uint32_t j = c * spc; j < (c + 1) * spc; ++j) sum += __popc(fm[j]);
+          const uint64_t k = k_base + lane * per_lane + c;
+          if (k < a.n_chunks) a.counts[k] = sum;
         }
       }
     }
+    if (a.counts_mode == 2 && total) {
+      const uint64_t last = min(tile_e0 + TILE, n) - 1;
+      const uint64_t k0 = tile_e0 / a.chunk;
+      if (k0 == last / a.chunk) {
+        if (lane == 0) atomicAdd(&a.counts[k0], total);
+      } else {
+        for (int j = 0; j < SPL; ++j) {
+          uint32_t m = fm[j];
+          const uint64_t e0 = tile_e0 + static_cast<uint64_t>(lane * SPL + j) * EPV;
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            atomicAdd(&a.counts[(e0 + b) / a.chunk], 1u);
+          }
+        }
+      }
+    }
+
+    // tile-local escape records, ascending element order, into the scratch slot
+    const uint32_t n_rec = S.esc_n[q];
+    if (total && total <= kEscCap && n_rec == total) {
+      uint32_t run = excl_lane;
+      for (int j = 0; j < SPL; ++j) {
+        sp[lane * SPL + j] = static_cast<uint16_t>(run);
+        run += __popc(fm[j]);
+      }
+      __syncwarp();
+      uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
+      uint8_t* sval = a.scr_val + tile * kEscCap;
+      for (uint32_t r = lane; r < n_rec; r += 32) {
+        const uint32_t rec = S.esc_rec[q][r];
+        const uint32_t local = rec & 0xFFFFu, slot = local / EPV, b = local % EPV;
+        const uint32_t rank = sp[slot] + __popc(S.fmask[q][slot] & ((1u << b) - 1u));
+        sval[rank] = static_cast<uint8_t>(rec >> 16);
+        put_position<POSB>(spos, rank, tile_e0 + local, a.chunk, a.chunk_shift);
+      }
+    }
+    // (tiles with more than kEscCap escapes are re-derived by escape_gather)
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (lane == 0) {
+      S.esc_n[q] = 0;
+      mbar_arrive(&S.scan_empty[q]);
+    }
+    t_work += clock64() - c1;
+  }
+  if (a.dbg && lane == 0) {
+    atomicAdd(&a.dbg[2], static_cast<unsigned long long>(t_wait));
+    atomicAdd(&a.dbg[3], static_cast<unsigned long long>(t_work));
+  }
+}
+
+// ------------------------------------------------------------------ K2b
+struct GatherArgs {
+  const uint8_t* words;
+  uint64_t n;
+  const uint32_t* tile_esc;
+  const uint8_t* scr_pos;
+  const uint8_t* scr_val;
+  uint64_t num_tiles;
+  uint64_t tile_elems;
+  uint8_t* positions;
+  uint8_t* values;
+  uint64_t capacity;
+  uint64_t* n_escapes;
+  uint64_t* states;
+  unsigned long long* counter;
+  uint64_t num_groups;
+  uint32_t chunk;
+  int32_t chunk_shift;
+};
+
+constexpr int kGatherTiles = 32;  // tiles per CTA (one warp handles 4)
+
+template <int FMT, int POSB>
+__global__ void __launch_bounds__(kThreads)
+    escape_gather(const __grid_constant__ sz_params p, const GatherArgs a) {
+  constexpr int PB = POSB == 0 ? 1 : POSB;
+  constexpr int WB = Fmt<FMT>::kWordBytes;
+  __shared__ uint64_t tpref[kGatherTiles];
+  __shared__ uint32_t tcnt[kGatherTiles];
+  __shared__ unsigned long long s_group;
+  __shared__ uint8_t lut[256];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 256; i += kThreads) lut[i] = p.enc_lut[i];
+  if (tid == 0) s_group = atomicAdd(a.counter, 1ull);
+  __syncthreads();
+  const uint64_t group = s_group;
+  const uint64_t t0 = group * kGatherTiles;
+  if (warp == 0) {
+    const uint64_t t = t0 + lane;
+    const uint32_t c = t < a.num_tiles ? a.tile_esc[t] : 0u;
+    uint64_t incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const uint64_t agg = __shfl_sync(0xffffffffu, incl, 31);
+    const uint64_t ex = lookback_warp(a.states, group, agg);
+    tpref[lane] = ex + incl - c;
+    tcnt[lane] = c;
+    if (lane == 0 && group == a.num_groups - 1) *a.n_escapes = ex + agg;
+  }
+  __syncthreads();
+  for (int k = warp; k < kGatherTiles; k += kWarps) {
+    const uint64_t tile = t0 + k;
+    if (tile >= a.num_tiles) break;
+    const uint32_t c = tcnt[k];
+    if (!c) continue;
+    const uint64_t base = tpref[k];
+    if (c <= kEscCap) {
+      const uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
+      const uint8_t* sval = a.scr_val + tile * kEscCap;
+      for (uint32_t r = lane; r < c; r += 32) {
+        const uint64_t o = base + r;
+        if (o >= a.capacity) break;
+        a.values[o] = sval[r];
+        if constexpr (POSB == 1) a.positions[o] = spos[r];
+        else if constexpr (POSB == 2)
+          reinterpret_cast<uint16_t*>(a.positions)[o] = reinterpret_cast<const uint16_t*>(spos)[r];
+        else if constexpr (POSB == 4)
+          reinterpret_cast<uint32_t*>(a.positions)[o] = reinterpret_cast<const uint32_t*>(spos)[r];
+      }
+    } else {
+      // escape-heavy tile: walk its words in element order (ballot ranks)
+      const uint64_t e_begin = tile * a.tile_elems;
+      const uint64_t e_end = min(e_begin + a.tile_elems, a.n);
+      uint64_t ord = base;
+      for (uint64_t e = e_begin; e < e_end; e += 32) {
+        const uint64_t idx = e + lane;
+        uint32_t ev = 0;
+        bool esc = false;
+        if (idx < e_end) {
+          const uint32_t w = WB == 2 ? reinterpret_cast<const uint16_t*>(a.words)[idx] : a.words[idx];
+          ev = raw_exponent<FMT>(w);
+          esc = (lut[ev] & 0x10) != 0;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, esc);
+        if (esc) {
+          const uint64_t o = ord + __popc(bal & ((1u << lane) - 1u));
+          if (o < a.capacity) {
+            a.values[o] = static_cast<uint8_t>(ev);
+            put_position<POSB>(a.positions, o, idx, a.chunk, a.chunk_shift);
+          }
+        }
+        ord += __popc(bal);
+      }
+    }
   }
 }
 
@@ -379,6 +575,47 @@ using namespace sz;
 uint64_t encode_tile_for(uint32_t fmt) {
   return static_cast<uint64_t>(kEncSlots) * (fmt == SZ_BF16 ? 16 : 32);
 }
+int pos_bytes(const sz_params* p) {
+  return p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
+}
+
+// Workspace layout (all offsets 256-byte aligned):
+//   [tile counter | gather counter | gather look-back states]  -> zeroed per call
+//   tile_esc[num_tiles] u32, scratch positions, scratch values
+struct EncWs {
+  unsigned long long* tile_counter;
+  unsigned long long* gather_counter;
+  uint64_t* states;
+  uint32_t* tile_esc;
+  uint8_t* scr_pos;
+  uint8_t* scr_val;
+  size_t zero_bytes;
+  size_t total;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+EncWs carve(void* base, uint64_t n, const sz_params* p) {
+  EncWs w{};
+  const uint64_t tiles = (n + encode_tile_for(p->fmt) - 1) / encode_tile_for(p->fmt);
+  const uint64_t groups = (tiles + kGatherTiles - 1) / kGatherTiles;
+  const int pb = pos_bytes(p) ? pos_bytes(p) : 1;
+  uint8_t* b = static_cast<uint8_t*>(base);
+  size_t off = 0;
+  w.tile_counter = reinterpret_cast<unsigned long long*>(b + off);
+  w.gather_counter = w.tile_counter + 1;
+  w.states = reinterpret_cast<uint64_t*>(w.tile_counter + 2);
+  off = align256((2 + groups) * sizeof(uint64_t));
+  w.zero_bytes = off;
+  w.tile_esc = reinterpret_cast<uint32_t*>(b + off);
+  off = align256(off + tiles * sizeof(uint32_t));
+  w.scr_pos = b + off;
+  off = align256(off + tiles * kEscCap * pb);
+  w.scr_val = b + off;
+  off = align256(off + tiles * kEscCap);
+  w.total = off;
+  return w;
+}
 
 int sm_count() {
   int dev = 0, sms = 148;
@@ -388,34 +625,37 @@ int sm_count() {
 }
 
 template <int FMT, int CB, int POSB>
-cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
-  auto kern = encode_kernel<FMT, CB, POSB>;
+cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
+                          cudaStream_t s) {
+  auto kern = encode_tiles<FMT, CB, POSB>;
   const int smem = static_cast<int>(sizeof(EncSmem));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEncThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t want = static_cast<uint64_t>(sm_count()) * per_sm;
+  const uint64_t want = static_cast<uint64_t>(sm_count());
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
   kern<<<grid, kEncThreads, smem, s>>>(p, a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups), kThreads, 0, s>>>(p, g);
   return cudaGetLastError();
 }
 
 template <int FMT, int CB>
-cudaError_t dispatch_pos(int posb, const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
+cudaError_t dispatch_pos(int posb, const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
+                         cudaStream_t s) {
   switch (posb) {
-    case 0: return launch_encode<FMT, CB, 0>(p, a, s);
-    case 1: return launch_encode<FMT, CB, 1>(p, a, s);
-    case 2: return launch_encode<FMT, CB, 2>(p, a, s);
-    default: return launch_encode<FMT, CB, 4>(p, a, s);
+    case 0: return launch_encode<FMT, CB, 0>(p, a, g, s);
+    case 1: return launch_encode<FMT, CB, 1>(p, a, g, s);
+    case 2: return launch_encode<FMT, CB, 2>(p, a, g, s);
+    default: return launch_encode<FMT, CB, 4>(p, a, g, s);
   }
 }
 
 template <int FMT>
-cudaError_t dispatch_cb(int posb, const sz_params& p, const EncodeArgs& a, cudaStream_t s) {
-  return p.code_bits == 4 ? dispatch_pos<FMT, 4>(posb, p, a, s)
-                          : dispatch_pos<FMT, 3>(posb, p, a, s);
+cudaError_t dispatch_cb(int posb, const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
+                        cudaStream_t s) {
+  return p.code_bits == 4 ? dispatch_pos<FMT, 4>(posb, p, a, g, s)
+                          : dispatch_pos<FMT, 3>(posb, p, a, g, s);
 }
 
 }  // namespace
@@ -427,8 +667,7 @@ int sz_check_params(const sz_params* p, int decode_side);
 
 size_t sz_encode_workspace_bytes(uint64_t n, const sz_params* p) {
   if (!p || p->fmt > SZ_E4M3) return 0;
-  const uint64_t tiles = (n + encode_tile_for(p->fmt) - 1) / encode_tile_for(p->fmt);
-  return static_cast<size_t>((tiles + 1) * sizeof(uint64_t) + 256);
+  return carve(nullptr, n, p).total + 256;
 }
 
 int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_encoded* out,
@@ -437,7 +676,7 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
   if (n == 0 || !out || !d_words) return SZ_ECONFIG;
   if ((reinterpret_cast<uintptr_t>(d_words) & 31) ||
       (reinterpret_cast<uintptr_t>(out->d_codes) & 15) ||
-      (reinterpret_cast<uintptr_t>(out->d_sm) & 15))
+      (reinterpret_cast<uintptr_t>(out->d_sm) & 15) || (reinterpret_cast<uintptr_t>(d_ws) & 255))
     return SZ_EALIGN;
   if (ws_bytes < sz_encode_workspace_bytes(n, p)) return SZ_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -446,6 +685,7 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
   const bool chunked = !p->sentinel && !p->abs32;
   const int epv = p->fmt == SZ_BF16 ? 16 : 32;
   const uint64_t tile = encode_tile_for(p->fmt);
+  const EncWs w = carve(d_ws, n, p);
 
   EncodeArgs a{};
   a.words = static_cast<const uint8_t*>(d_words);
@@ -453,40 +693,75 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
   a.codes = static_cast<uint8_t*>(out->d_codes);
   a.sm = static_cast<uint8_t*>(out->d_sm);
   a.counts = out->d_counts;
-  a.positions = out->d_positions;
-  a.values = out->d_values;
-  a.n_escapes = out->d_n_escapes;
-  a.capacity = out->escape_capacity;
   a.num_tiles = (n + tile - 1) / tile;
-  a.states = static_cast<uint64_t*>(d_ws);
-  a.tile_counter = reinterpret_cast<unsigned long long*>(a.states + a.num_tiles);
   a.n_chunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size : 0;
   a.codes_len = (n * p->code_bits + 7) / 8;
   a.sm_len = (n * sm_bits + 7) / 8;
   a.chunk = p->chunk_size;
   a.chunk_shift = (p->chunk_size & (p->chunk_size - 1)) == 0 ? __builtin_ctz(p->chunk_size) : -1;
   a.counts_mode = 0;
+  a.tile_counter = w.tile_counter;
+  a.tile_esc = w.tile_esc;
+  a.scr_pos = w.scr_pos;
+  a.scr_val = w.scr_val;
   if (chunked) {
     if (!out->d_counts) return SZ_ECONFIG;
     a.counts_mode = (tile % p->chunk_size == 0 && p->chunk_size % epv == 0) ? 1 : 2;
   }
-  if (a.capacity && (!out->d_values || (!p->sentinel && !out->d_positions))) return SZ_ECONFIG;
+  if (out->escape_capacity && (!out->d_values || (!p->sentinel && !out->d_positions)))
+    return SZ_ECONFIG;
 
-  cudaError_t e = cudaMemsetAsync(d_ws, 0, (a.num_tiles + 1) * sizeof(uint64_t), s);
+  GatherArgs g{};
+  g.words = a.words;
+  g.n = n;
+  g.tile_esc = w.tile_esc;
+  g.scr_pos = w.scr_pos;
+  g.scr_val = w.scr_val;
+  g.num_tiles = a.num_tiles;
+  g.tile_elems = tile;
+  g.positions = static_cast<uint8_t*>(out->d_positions);
+  g.values = out->d_values;
+  g.capacity = out->escape_capacity;
+  g.n_escapes = out->d_n_escapes;
+  g.states = w.states;
+  g.counter = w.gather_counter;
+  g.num_groups = (a.num_tiles + kGatherTiles - 1) / kGatherTiles;
+  g.chunk = a.chunk;
+  g.chunk_shift = a.chunk_shift;
+
+  cudaError_t e = cudaMemsetAsync(d_ws, 0, w.zero_bytes, s);
   if (e == cudaSuccess && a.counts_mode == 2)
     e = cudaMemsetAsync(out->d_counts, 0, a.n_chunks * sizeof(uint32_t), s);
   if (e != cudaSuccess) return sz_record_cuda(e);
 
-  const int posb = p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
+  static const bool dbg_timers = std::getenv("SZ_DEBUG_TIMERS") != nullptr;
+  unsigned long long* dbg = nullptr;
+  if (dbg_timers) {
+    cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s);
+    a.dbg = dbg;
+  }
+  const int posb = pos_bytes(p);
   switch (p->fmt) {
-    case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, s); break;
-    case SZ_E5M2: e = dispatch_cb<SZ_E5M2>(posb, *p, a, s); break;
-    default: e = dispatch_cb<SZ_E4M3>(posb, *p, a, s); break;
+    case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, g, s); break;
+    case SZ_E5M2: e = dispatch_cb<SZ_E5M2>(posb, *p, a, g, s); break;
+    default: e = dispatch_cb<SZ_E4M3>(posb, *p, a, g, s); break;
   }
   if (e != cudaSuccess) return sz_record_cuda(e);
-  if (exp_bits != 8 && a.capacity) {
+  if (dbg) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr,
+                 "[sz_encode timers] dense wait=%llu work=%llu | writer wait=%llu work=%llu"
+                 " | producer in_empty=%llu scan_empty=%llu\n",
+                 h[0], h[1], h[2], h[3], h[6], h[7]);
+    cudaFree(dbg);
+  }
+  if (exp_bits != 8 && out->escape_capacity) {
     if (!out->d_values_packed) return SZ_ECONFIG;
-    pack_values_kernel<<<296, kThreads, 0, s>>>(a.values, a.n_escapes, a.capacity, exp_bits,
+    pack_values_kernel<<<296, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
+                                                out->escape_capacity, exp_bits,
                                                 out->d_values_packed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);

@@ -111,7 +111,7 @@ class DeviceCodec:
     def check_status(self) -> None:
         """Synchronise and raise CorruptionError if the last decode failed."""
         raw = self.status.cpu().numpy()
-        _raise_from_status(raw, self.streams(), self.config, self.codebook, self.bufs.codes)
+        _raise_from_status(raw, self.streams(), self.config, self.codebook, self.bufs.values)
 
     # ------------------------------------------------------------ compare
     def compare(self, a: torch.Tensor, b: torch.Tensor, stream=None) -> torch.Tensor:

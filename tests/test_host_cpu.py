@@ -47,7 +47,7 @@ def test_workspace_queries_need_no_gpu():
                                                     4, m.CodebookMode.TOPK_EXPLICIT))
     from paper_2605_01708_b200.codec import _config_params
     p = _config_params(cfg, cfg.codebook)
-    assert lib.sz_encode_workspace_bytes(1 << 31, p) >= (1 << 31) // 8192 * 8
+    assert lib.sz_encode_workspace_bytes(1 << 31, p) >= (1 << 31) // 16384 * 8
     assert lib.sz_decode_workspace_bytes(1 << 31, 0, p) >= ((1 << 31) // 1024 + 1) * 8
 
 
