@@ -51,6 +51,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
     BUILD.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_v else []
+    # e.g. SZ_NVCC_DEFINES="SZ_TIMERS" for the per-role pipeline timers
+    extra += [f"-D{d}" for d in os.environ.get("SZ_NVCC_DEFINES", "").split() if d]
 
     def compile_one(src: Path) -> tuple[Path, str]:
         obj = BUILD / (src.stem + ".o")

@@ -13,6 +13,14 @@
 
 #include "../../include/splitzip_b200.h"
 
+// Per-role cycle counters for pipeline tuning (build with -DSZ_TIMERS and run
+// with SZ_DEBUG_TIMERS=1); compiled out otherwise.
+#ifdef SZ_TIMERS
+#define SZ_CLOCK() clock64()
+#else
+#define SZ_CLOCK() 0ll
+#endif
+
 namespace sz {
 
 constexpr int kThreads = 256;          // CTA size of every streaming kernel
@@ -313,8 +321,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the
+// phase completes (or the hint expires) instead of spinning on issue slots.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
   }
 }
 // 1-D bulk copy global -> shared (TMA engine, UBLKCP), completion counted in

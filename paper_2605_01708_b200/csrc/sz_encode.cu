@@ -116,9 +116,12 @@ __device__ __forceinline__ uint32_t raw_exponent(uint32_t word) {
 }
 
 // Dense transform of one 32-byte slot; returns the slot's escape bitmask.
-template <int FMT, int CB>
+// TAIL=false is the steady-state path (slot fully inside N, stores at the
+// precomputed slot addresses); TAIL=true handles the ragged last slots.
+template <int FMT, int CB, bool TAIL>
 __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const uint8_t* lut,
-                                                int nv, const EncodeArgs& a, uint64_t e0) {
+                                                int nv, uint8_t* cdst, uint8_t* sdst,
+                                                const EncodeArgs& a, uint64_t e0) {
   constexpr int EPV = kEpv<FMT>;
   constexpr int G = EPV / 4;
   constexpr int SMB = Fmt<FMT>::kSmBits;
@@ -133,7 +136,7 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
     uint32_t e4, a4;
     split_group<FMT>(x, g, e4, a4);
     uint32_t m4 = lut4(lut, e4);
-    if (nv < EPV) {  // tail slot: zero codes, flags and SM beyond N
+    if (TAIL && nv < EPV) {  // tail slot: zero codes, flags and SM beyond N
       const int v = min(max(nv - 4 * g, 0), 4);
       const uint32_t keep = v >= 4 ? 0xFFFFFFFFu : ((1u << (8 * v)) - 1u);
       m4 &= keep;
@@ -176,13 +179,12 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
       concat_groups<G, 12>(grp, sw);
     }
   }
-  const uint64_t coff = e0 * CB / 8, soff = e0 * SMB / 8;
-  if (nv == EPV) {
-    st_packed<CBYTES>(a.codes + coff, cw);
-    st_packed<SBYTES>(a.sm + soff, sw);
+  if (!TAIL || nv == EPV) {
+    st_packed<CBYTES>(cdst, cw);
+    st_packed<SBYTES>(sdst, sw);
   } else if (nv > 0) {
-    st_bytes_clipped<CBYTES>(a.codes, coff, cw, a.codes_len);
-    st_bytes_clipped<SBYTES>(a.sm, soff, sw, a.sm_len);
+    st_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, a.codes_len);
+    st_bytes_clipped<SBYTES>(a.sm, e0 * SMB / 8, sw, a.sm_len);
   }
   return fm;
 }
@@ -206,6 +208,9 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   constexpr int EPV = kEpv<FMT>;
   constexpr int WB = Fmt<FMT>::kWordBytes;
   constexpr uint64_t TILE = static_cast<uint64_t>(kEncSlots) * EPV;
+  constexpr int SMB = Fmt<FMT>::kSmBits;
+  constexpr int CBYTES = EPV * CB / 8;
+  constexpr int SBYTES = EPV * SMB / 8;
   constexpr int PB = POSB == 0 ? 1 : POSB;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   EncSmem& S = *reinterpret_cast<EncSmem*>(smem_raw);
@@ -234,12 +239,12 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       for (uint32_t it = 0;; ++it) {
         const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
         const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
-        const long long c0 = clock64();
+        const long long c0 = SZ_CLOCK();
         mbar_wait(&S.in_empty[s], sph ^ 1);
-        const long long c1 = clock64();
+        const long long c1 = SZ_CLOCK();
         mbar_wait(&S.scan_empty[q], qph ^ 1);
         t_in += c1 - c0;
-        t_scan += clock64() - c1;
+        t_scan += SZ_CLOCK() - c1;
         const uint64_t tile = atomicAdd(a.tile_counter, 1ull);
         if (tile >= a.num_tiles) {
           // end markers in this slot and the next kWriterWarps-1 (one per
@@ -278,9 +283,9 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
       const uint32_t q = it % kEncScanSlots;
-      const long long c0 = clock64();
+      const long long c0 = SZ_CLOCK();
       mbar_wait(&S.full[s], sph);
-      const long long c1 = clock64();
+      const long long c1 = SZ_CLOCK();
       t_wait += c1 - c0;
       const uint64_t tile = S.meta[q];
       if (tile == ~0ull) {
@@ -289,13 +294,16 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         break;
       }
       const uint64_t tile_e0 = tile * TILE;
+      const bool tail_tile = tile_e0 + TILE > n;
+      uint8_t* const ctile = a.codes + tile_e0 * CB / 8;
+      uint8_t* const stile = a.sm + tile_e0 * SMB / 8;
       uint32_t x[kEncItems][8];
       int nv[kEncItems];
 #pragma unroll
       for (int i = 0; i < kEncItems; ++i) {
         const int slot = i * kEncDense + tid;
         const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
-        nv[i] = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
+        nv[i] = !tail_tile || e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
         if (nv[i] == EPV) {
           const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + slot * 32);
           const uint4 v0 = src[0], v1 = src[1];
@@ -309,8 +317,15 @@ __global__ void __launch_bounds__(kEncThreads, 1)
 #pragma unroll
       for (int i = 0; i < kEncItems; ++i) {
         const int slot = i * kEncDense + tid;
-        const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
-        const uint32_t fm = encode_slot<FMT, CB>(x[i], S.lut, nv[i], a, e0);
+        uint32_t fm;
+        if (!tail_tile) {
+          fm = encode_slot<FMT, CB, false>(x[i], S.lut, EPV, ctile + slot * CBYTES,
+                                           stile + slot * SBYTES, a, 0);
+        } else {
+          fm = encode_slot<FMT, CB, true>(x[i], S.lut, nv[i], ctile + slot * CBYTES,
+                                          stile + slot * SBYTES, a,
+                                          tile_e0 + static_cast<uint64_t>(slot) * EPV);
+        }
         S.fmask[q][slot] = fm;
         if (fm) {  // rare: append (element, raw exponent) records for the writer
           uint32_t r = atomicAdd(&S.esc_n[q], static_cast<uint32_t>(__popc(fm)));
@@ -329,7 +344,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         }
       }
       mbar_arrive(&S.computed[q]);
-      t_work += clock64() - c1;
+      t_work += SZ_CLOCK() - c1;
     }
     if (a.dbg && lane == 0) {
       atomicAdd(&a.dbg[0], static_cast<unsigned long long>(t_wait));
@@ -345,9 +360,9 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   long long t_wait = 0, t_work = 0;
   for (uint32_t it = ww;; it += kWriterWarps) {
     const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
-    const long long c0 = clock64();
+    const long long c0 = SZ_CLOCK();
     mbar_wait(&S.computed[q], qph);
-    const long long c1 = clock64();
+    const long long c1 = SZ_CLOCK();
     t_wait += c1 - c0;
     const uint64_t tile = S.meta[q];
     if (tile == ~0ull) break;
@@ -434,7 +449,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       S.esc_n[q] = 0;
       mbar_arrive(&S.scan_empty[q]);
     }
-    t_work += clock64() - c1;
+    t_work += SZ_CLOCK() - c1;
   }
   if (a.dbg && lane == 0) {
     atomicAdd(&a.dbg[2], static_cast<unsigned long long>(t_wait));
@@ -495,25 +510,39 @@ __global__ void __launch_bounds__(kThreads)
     if (lane == 0 && group == a.num_groups - 1) *a.n_escapes = ex + agg;
   }
   __syncthreads();
+  // Flat pass over every record of the group's regular tiles: thread t moves
+  // records t, t+256, ... (tile found by a search over the 32 local prefixes),
+  // so all loads of the group are in flight at once.
+  {
+    const uint64_t g_base = tpref[0];
+    const uint64_t g_total = tpref[kGatherTiles - 1] + tcnt[kGatherTiles - 1] - g_base;
+    for (uint64_t r = tid; r < g_total; r += kThreads) {
+      const uint64_t o = g_base + r;
+      int lo = 0, hi = kGatherTiles;  // last k with tpref[k] <= o
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (tpref[mid] <= o) lo = mid; else hi = mid;
+      }
+      const uint32_t c = tcnt[lo];
+      if (c > kEscCap || o >= a.capacity) continue;
+      const uint64_t tile = t0 + lo;
+      const uint64_t rr = o - tpref[lo];
+      a.values[o] = a.scr_val[tile * kEscCap + rr];
+      const uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
+      if constexpr (POSB == 1) a.positions[o] = spos[rr];
+      else if constexpr (POSB == 2)
+        reinterpret_cast<uint16_t*>(a.positions)[o] = reinterpret_cast<const uint16_t*>(spos)[rr];
+      else if constexpr (POSB == 4)
+        reinterpret_cast<uint32_t*>(a.positions)[o] = reinterpret_cast<const uint32_t*>(spos)[rr];
+    }
+  }
   for (int k = warp; k < kGatherTiles; k += kWarps) {
     const uint64_t tile = t0 + k;
     if (tile >= a.num_tiles) break;
     const uint32_t c = tcnt[k];
-    if (!c) continue;
     const uint64_t base = tpref[k];
     if (c <= kEscCap) {
-      const uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
-      const uint8_t* sval = a.scr_val + tile * kEscCap;
-      for (uint32_t r = lane; r < c; r += 32) {
-        const uint64_t o = base + r;
-        if (o >= a.capacity) break;
-        a.values[o] = sval[r];
-        if constexpr (POSB == 1) a.positions[o] = spos[r];
-        else if constexpr (POSB == 2)
-          reinterpret_cast<uint16_t*>(a.positions)[o] = reinterpret_cast<const uint16_t*>(spos)[r];
-        else if constexpr (POSB == 4)
-          reinterpret_cast<uint32_t*>(a.positions)[o] = reinterpret_cast<const uint32_t*>(spos)[r];
-      }
+      continue;  // moved by the flat pass above
     } else {
       // escape-heavy tile: walk its words in element order (ballot ranks)
       const uint64_t e_begin = tile * a.tile_elems;
@@ -734,7 +763,11 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
     e = cudaMemsetAsync(out->d_counts, 0, a.n_chunks * sizeof(uint32_t), s);
   if (e != cudaSuccess) return sz_record_cuda(e);
 
+#ifdef SZ_TIMERS
   static const bool dbg_timers = std::getenv("SZ_DEBUG_TIMERS") != nullptr;
+#else
+  constexpr bool dbg_timers = false;  // build with -DSZ_TIMERS for role timers
+#endif
   unsigned long long* dbg = nullptr;
   if (dbg_timers) {
     cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
