@@ -83,6 +83,13 @@ typedef struct sz_encoded {
   uint8_t* d_values_packed;
   uint64_t* d_n_escapes;
   uint64_t escape_capacity;
+  /* Optional append mode for chunk-aligned pieces of one stream: when
+   * non-NULL, this call's escapes are written at ordinals *d_escape_base + i
+   * (capacity applies to the absolute ordinal) and *d_escape_base is advanced
+   * by this call's M, all on the device — so a piecewise host<->device
+   * pipeline builds the global escape stream without host round trips
+   * (chunk-relative sections of chunk-aligned pieces concatenate exactly). */
+  uint64_t* d_escape_base;
 } sz_encoded;
 
 /* Decode inputs: the same sections, read-only, plus the declared counts. */

@@ -37,7 +37,7 @@ class SzEncoded(C.Structure):
     _fields_ = [("d_codes", C.c_void_p), ("d_sm", C.c_void_p), ("d_counts", C.c_void_p),
                 ("d_positions", C.c_void_p), ("d_values", C.c_void_p),
                 ("d_values_packed", C.c_void_p), ("d_n_escapes", C.c_void_p),
-                ("escape_capacity", C.c_uint64)]
+                ("escape_capacity", C.c_uint64), ("d_escape_base", C.c_void_p)]
 
 
 class SzEncodedIn(C.Structure):

@@ -234,7 +234,8 @@ class EncodedStreams:
                 + packed_nbytes(m, self.codebook.fmt.exp_bits))
 
     def to_host(self) -> "EncodedStreams":
-        if not self.on_device:
+        """Reference-typed copy (bytes planes, numpy arrays) of tensor sections."""
+        if not isinstance(self.packed_codes, torch.Tensor):
             return self
         pos = to_numpy(self.escape_positions)
         return EncodedStreams(
@@ -303,6 +304,7 @@ class EncodeBuffers:
         s.d_values_packed = N.ptr(self.values_packed)
         s.d_n_escapes = N.ptr(self.m)
         s.escape_capacity = self.capacity
+        s.d_escape_base = None
         return s
 
 
@@ -331,6 +333,13 @@ def encode(stream: RawTensorStream, config: CodecConfig, *,
            capacity: int | None = None) -> EncodedStreams:
     """Compress a stream; :func:`decode` inverts it bit-exactly (codec.py:299-321)."""
     _check_stream(stream, config)
+    if not stream.on_device and config.codebook is not None:
+        from . import hostpipe
+        if hostpipe.pipelinable(config, stream.n_elements):
+            # host-resident stream: piecewise H2D / K2 / D2H overlap
+            words_h = hostpipe.host_tensor(stream.words, config.fmt.torch_dtype)
+            enc = hostpipe.encode_host(words_h, config, config.codebook, capacity)
+            return enc if isinstance(stream.words, torch.Tensor) else enc.to_host()
     words = stream.device_words()
     codebook = config.codebook or _dynamic_codebook(words, config)
     params = _config_params(config, codebook)
@@ -490,6 +499,16 @@ def decode(streams: EncodedStreams, config: CodecConfig,
             _raise_values(first, streams, config)
         raise CorruptionError(msg)
 
+    if not is_device(streams.packed_codes):
+        from . import hostpipe
+        if hostpipe.pipelinable(config, n):
+            counts_np = to_numpy(streams.chunk_counts)
+            if int(counts_np.astype(np.int64).sum()) == m:
+                out_h = hostpipe.decode_host(streams, config, codebook, counts_np)
+                if out_h is not None:
+                    keep_torch = isinstance(streams.packed_codes, torch.Tensor)
+                    return RawTensorStream(fmt, out_h if keep_torch else out_h.numpy())
+            # inconsistent or corrupt: the monolithic path below raises exactly
     lib = N.load_library()
     codes = to_device(streams.packed_codes, torch.uint8, align=16)
     sm = to_device(streams.sign_mantissa, torch.uint8, align=16)

@@ -65,6 +65,8 @@ struct EncodeArgs {
   uint32_t* tile_esc;    // per-tile escape count
   uint8_t* scr_pos;      // kEscCap positions per tile (POSB bytes each)
   uint8_t* scr_val;      // kEscCap raw exponents per tile
+  const uint64_t* escape_base;  // append mode: global ordinal offset (or null)
+  uint64_t* base_snapshot;      // workspace copy of *escape_base for K2b
   unsigned long long* dbg;  // optional per-role cycle counters (SZ_DEBUG_TIMERS)
 };
 
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
   for (int i = tid; i < 256; i += kEncThreads) S.lut[i] = p.enc_lut[i];
+  if (blockIdx.x == 0 && tid == 0) *a.base_snapshot = a.escape_base ? *a.escape_base : 0;
   if (tid == 0) {
     for (int s = 0; s < kEncInStages; ++s) {
       mbar_init(&S.full[s], 1);
@@ -475,6 +478,8 @@ struct GatherArgs {
   uint64_t num_groups;
   uint32_t chunk;
   int32_t chunk_shift;
+  const uint64_t* base_snapshot;  // append offset captured by K2a
+  uint64_t* escape_base;          // append mode: advanced by this call's M
 };
 
 constexpr int kGatherTiles = 32;  // tiles per CTA (one warp handles 4)
@@ -505,9 +510,13 @@ __global__ void __launch_bounds__(kThreads)
     }
     const uint64_t agg = __shfl_sync(0xffffffffu, incl, 31);
     const uint64_t ex = lookback_warp(a.states, group, agg);
-    tpref[lane] = ex + incl - c;
+    const uint64_t base = *a.base_snapshot;
+    tpref[lane] = base + ex + incl - c;
     tcnt[lane] = c;
-    if (lane == 0 && group == a.num_groups - 1) *a.n_escapes = ex + agg;
+    if (lane == 0 && group == a.num_groups - 1) {
+      *a.n_escapes = ex + agg;
+      if (a.escape_base) *a.escape_base = base + ex + agg;
+    }
   }
   __syncthreads();
   // Flat pass over every record of the group's regular tiles: thread t moves
@@ -614,6 +623,7 @@ int pos_bytes(const sz_params* p) {
 struct EncWs {
   unsigned long long* tile_counter;
   unsigned long long* gather_counter;
+  uint64_t* snapshot;
   uint64_t* states;
   uint32_t* tile_esc;
   uint8_t* scr_pos;
@@ -633,8 +643,9 @@ EncWs carve(void* base, uint64_t n, const sz_params* p) {
   size_t off = 0;
   w.tile_counter = reinterpret_cast<unsigned long long*>(b + off);
   w.gather_counter = w.tile_counter + 1;
-  w.states = reinterpret_cast<uint64_t*>(w.tile_counter + 2);
-  off = align256((2 + groups) * sizeof(uint64_t));
+  w.snapshot = reinterpret_cast<uint64_t*>(w.tile_counter + 2);
+  w.states = reinterpret_cast<uint64_t*>(w.tile_counter + 3);
+  off = align256((3 + groups) * sizeof(uint64_t));
   w.zero_bytes = off;
   w.tile_esc = reinterpret_cast<uint32_t*>(b + off);
   off = align256(off + tiles * sizeof(uint32_t));
@@ -733,6 +744,8 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
   a.tile_esc = w.tile_esc;
   a.scr_pos = w.scr_pos;
   a.scr_val = w.scr_val;
+  a.escape_base = out->d_escape_base;
+  a.base_snapshot = w.snapshot;
   if (chunked) {
     if (!out->d_counts) return SZ_ECONFIG;
     a.counts_mode = (tile % p->chunk_size == 0 && p->chunk_size % epv == 0) ? 1 : 2;
@@ -757,6 +770,8 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
   g.num_groups = (a.num_tiles + kGatherTiles - 1) / kGatherTiles;
   g.chunk = a.chunk;
   g.chunk_shift = a.chunk_shift;
+  g.base_snapshot = w.snapshot;
+  g.escape_base = out->d_escape_base;
 
   cudaError_t e = cudaMemsetAsync(d_ws, 0, w.zero_bytes, s);
   if (e == cudaSuccess && a.counts_mode == 2)
@@ -791,7 +806,8 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
                  h[0], h[1], h[2], h[3], h[6], h[7]);
     cudaFree(dbg);
   }
-  if (exp_bits != 8 && out->escape_capacity) {
+  // (append mode: the caller packs the whole stream once, after the last piece)
+  if (exp_bits != 8 && out->escape_capacity && !out->d_escape_base) {
     if (!out->d_values_packed) return SZ_ECONFIG;
     pack_values_kernel<<<296, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
                                                 out->escape_capacity, exp_bits,

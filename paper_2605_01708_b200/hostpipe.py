@@ -1,0 +1,225 @@
+"""Piecewise host <-> device codec pipeline for host-resident streams.
+
+``encode``/``decode`` called on host data (numpy, bytes or CPU tensors) move
+every byte over PCIe.  Done naively (copy all, run, copy all back) the GPU
+idles during both copies.  This module cuts the stream into chunk-aligned
+pieces (chunk-relative sections of chunk-aligned pieces concatenate exactly:
+counts, code and sign|mantissa planes, positions; the escape ordinals are
+made global on the device by the encoder's append mode, ``d_escape_base``)
+and runs three CUDA streams — H2D copy, codec kernels, D2H copy — over two
+device buffers per plane, so PCIe in, the kernels and PCIe out overlap.
+Host outputs land directly in pinned buffers.
+"""
+
+from __future__ import annotations
+
+import math
+import warnings
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .calibration import ExponentCodebook
+from .codec import (CodecConfig, EncodedStreams, _config_params, _nbytes, default_capacity,
+                    packed_nbytes)
+from .formats import pack_bits_device
+
+PIECE_ELEMS = 1 << 26   # 128 MiB of BF16 per piece
+
+
+def piece_size(config: CodecConfig, n: int) -> int:
+    """Chunk-aligned piece length (multiple of the encoder tile where possible)."""
+    p = PIECE_ELEMS
+    if config.chunked and PIECE_ELEMS % config.chunk_size:
+        p = config.chunk_size * max(1, PIECE_ELEMS // config.chunk_size)
+    return p
+
+
+def pipelinable(config: CodecConfig, n: int) -> bool:
+    return config.chunked and n > piece_size(config, n)
+
+
+def host_tensor(x, dtype: torch.dtype) -> torch.Tensor:
+    """Zero-copy CPU tensor view of numpy / bytes / CPU tensor data."""
+    if isinstance(x, torch.Tensor):
+        t = x.reshape(-1)
+        return t if t.dtype == dtype else t.view(dtype)
+    if isinstance(x, (bytes, bytearray, memoryview)):
+        arr = np.frombuffer(x, dtype=np.uint8)
+    else:
+        arr = np.ascontiguousarray(np.asarray(x).reshape(-1))
+    np_dtype = {torch.uint8: np.uint8, torch.uint16: np.uint16, torch.uint32: np.uint32}[dtype]
+    if arr.dtype != np_dtype:
+        arr = arr.view(np_dtype) if arr.itemsize == np.dtype(np_dtype).itemsize else \
+            arr.astype(np_dtype)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # read-only buffers are only read
+        return torch.from_numpy(arr)
+
+
+class _Streams:
+    def __init__(self):
+        self.h2d = torch.cuda.Stream()
+        self.comp = torch.cuda.Stream()
+        self.d2h = torch.cuda.Stream()
+
+
+def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCodebook,
+                capacity: int | None = None) -> EncodedStreams:
+    """Encode a host stream piecewise; returns pinned CPU-tensor sections."""
+    lib = N.load_library()
+    dev = N.device()
+    fmt = config.fmt
+    n = words_h.numel()
+    P = piece_size(config, n)
+    npieces = -(-n // P)
+    params = _config_params(config, codebook)
+    cap = min(n, capacity if capacity is not None else default_capacity(n))
+    cb = config.code_bits
+
+    codes_h = torch.empty(packed_nbytes(n, cb), dtype=torch.uint8, pin_memory=True)
+    sm_h = torch.empty(config.sm_nbytes(n), dtype=torch.uint8, pin_memory=True)
+    counts_h = torch.empty(config.n_chunks(n), dtype=torch.uint32, pin_memory=True)
+    words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(2)]
+    codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(2)]
+    sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(2)]
+    cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(2)]
+    pos_d = torch.empty(cap, dtype=config.position_torch_dtype, device=dev)
+    val_d = torch.empty(cap, dtype=torch.uint8, device=dev)
+    base_d = torch.zeros(1, dtype=torch.int64, device=dev)
+    m_d = torch.empty(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(lib.sz_encode_workspace_bytes(P, params), dtype=torch.uint8, device=dev)
+
+    st = _Streams()
+    cur = torch.cuda.current_stream()
+    for s in (st.h2d, st.comp, st.d2h):
+        s.wait_stream(cur)
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_enc = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    for i in range(npieces):
+        b = i % 2
+        lo, hi = i * P, min(n, (i + 1) * P)
+        k = hi - lo
+        with torch.cuda.stream(st.h2d):
+            if i >= 2:
+                st.h2d.wait_event(ev_enc[b])
+            words_d[b][:k].copy_(words_h[lo:hi], non_blocking=True)
+            ev_h2d[b].record(st.h2d)
+        st.comp.wait_event(ev_h2d[b])
+        if i >= 2:
+            st.comp.wait_event(ev_d2h[b])
+        out = N.SzEncoded()
+        out.d_codes, out.d_sm = N.ptr(codes_d[b]), N.ptr(sm_d[b])
+        out.d_counts = N.ptr(cnt_d[b])
+        out.d_positions, out.d_values = N.ptr(pos_d), N.ptr(val_d)
+        out.d_values_packed = None
+        out.d_n_escapes = N.ptr(m_d)
+        out.escape_capacity = cap
+        out.d_escape_base = N.ptr(base_d)
+        N.check(lib.sz_encode(N.ptr(words_d[b]), k, params, out, N.ptr(ws), ws.numel(),
+                              st.comp.cuda_stream), "encode")
+        ev_enc[b].record(st.comp)
+        with torch.cuda.stream(st.d2h):
+            st.d2h.wait_event(ev_enc[b])
+            c0, c1 = packed_nbytes(lo, cb), packed_nbytes(hi, cb)
+            codes_h[c0:c1].copy_(codes_d[b][:c1 - c0], non_blocking=True)
+            s0, s1 = config.sm_nbytes(lo), config.sm_nbytes(hi)
+            sm_h[s0:s1].copy_(sm_d[b][:s1 - s0], non_blocking=True)
+            k0, k1 = config.n_chunks(lo), config.n_chunks(hi)
+            counts_h[k0:k1].copy_(cnt_d[b][:k1 - k0], non_blocking=True)
+            ev_d2h[b].record(st.d2h)
+    cur.wait_stream(st.d2h)
+    cur.wait_stream(st.comp)
+    m = int(base_d.cpu().numpy()[0])
+    if m > cap:  # overflow protocol: rerun with the exact escape count
+        return encode_host(words_h, config, codebook, capacity=m)
+    positions = pos_d[:m].to("cpu")
+    values = val_d[:m].to("cpu")
+    vp = None
+    if fmt.exp_bits != 8:
+        vp = pack_bits_device(val_d[:m], fmt.exp_bits).to("cpu")
+    return EncodedStreams(n, m, codes_h, sm_h, counts_h, positions, values, codebook, vp)
+
+
+def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: ExponentCodebook,
+                counts_np: np.ndarray) -> torch.Tensor | None:
+    """Decode host sections piecewise into a pinned CPU tensor.  Returns None
+    when any piece reports corruption (the caller re-runs the monolithic
+    decode, which raises with the reference's exact error order)."""
+    lib = N.load_library()
+    dev = N.device()
+    fmt = config.fmt
+    n, m = int(streams.n_elements), int(streams.n_escapes)
+    P = piece_size(config, n)
+    npieces = -(-n // P)
+    params = _config_params(config, codebook)
+    cb = config.code_bits
+    c = config.chunk_size
+
+    codes_h = host_tensor(streams.packed_codes, torch.uint8)
+    sm_h = host_tensor(streams.sign_mantissa, torch.uint8)
+    counts_h = host_tensor(counts_np.astype(np.uint32, copy=False), torch.uint32)
+    # ordinal offset of every piece = escapes in the chunks before it
+    prefix = np.concatenate([[0], np.cumsum(counts_np.astype(np.int64))])
+    out_h = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
+    codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(2)]
+    sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(2)]
+    cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(2)]
+    words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(2)]
+    status = torch.empty((npieces, N.STATUS_BYTES), dtype=torch.uint8, device=dev)
+    ws = [torch.empty(lib.sz_decode_workspace_bytes(P, 0, params), dtype=torch.uint8, device=dev)
+          for _ in range(2)]
+
+    st = _Streams()
+    cur = torch.cuda.current_stream()
+    for s in (st.h2d, st.comp, st.d2h):
+        s.wait_stream(cur)
+    with torch.cuda.stream(st.h2d):
+        pos_d = (host_tensor(streams.escape_positions, config.position_torch_dtype)
+                 .to(dev, non_blocking=True) if m else None)
+        val_d = host_tensor(streams.escape_values, torch.uint8).to(dev, non_blocking=True) \
+            if m else None
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_dec = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    pbytes = config.position_nbytes
+    for i in range(npieces):
+        b = i % 2
+        lo, hi = i * P, min(n, (i + 1) * P)
+        k = hi - lo
+        k0, k1 = lo // c, -(-hi // c)
+        o0, o1 = int(prefix[k0]), int(prefix[k1])
+        with torch.cuda.stream(st.h2d):
+            if i >= 2:
+                st.h2d.wait_event(ev_dec[b])
+            c0, c1 = packed_nbytes(lo, cb), packed_nbytes(hi, cb)
+            codes_d[b][:c1 - c0].copy_(codes_h[c0:c1], non_blocking=True)
+            s0, s1 = config.sm_nbytes(lo), config.sm_nbytes(hi)
+            sm_d[b][:s1 - s0].copy_(sm_h[s0:s1], non_blocking=True)
+            cnt_d[b][:k1 - k0].copy_(counts_h[k0:k1], non_blocking=True)
+            ev_h2d[b].record(st.h2d)
+        st.comp.wait_event(ev_h2d[b])
+        if i >= 2:
+            st.comp.wait_event(ev_d2h[b])
+        src = N.SzEncodedIn()
+        src.d_codes, src.d_sm = N.ptr(codes_d[b]), N.ptr(sm_d[b])
+        src.d_counts = N.ptr(cnt_d[b])
+        src.d_positions = (pos_d.data_ptr() + o0 * pbytes) if o1 > o0 else None
+        src.d_values = (val_d.data_ptr() + o0) if o1 > o0 else None
+        src.n_elements, src.n_escapes, src.n_counts = k, o1 - o0, k1 - k0
+        src.d_n_escapes = None
+        N.check(lib.sz_decode(src, params, N.ptr(words_d[b]), N.ptr(status[i]), N.ptr(ws[b]),
+                              ws[b].numel(), st.comp.cuda_stream), "decode")
+        ev_dec[b].record(st.comp)
+        with torch.cuda.stream(st.d2h):
+            st.d2h.wait_event(ev_dec[b])
+            out_h[lo:hi].copy_(words_d[b][:k], non_blocking=True)
+            ev_d2h[b].record(st.d2h)
+    cur.wait_stream(st.d2h)
+    cur.wait_stream(st.comp)
+    raw = status.cpu().numpy()
+    if raw.any():
+        return None
+    return out_h

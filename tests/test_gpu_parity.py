@@ -232,3 +232,44 @@ def test_random_lengths_roundtrip(seed):
         ref = O.encode(words, p, enc.codebook.entries)
         assert [b for _, b in enc.section_bytes()] == O.section_bytes(ref)
         assert m.verify_roundtrip(stream, cfg).ok
+
+
+@pytest.mark.parametrize("host_kind", ["numpy", "pinned", "pageable"])
+def test_host_pipeline_matches_oracle(host_kind, monkeypatch):
+    """Host-resident streams go through the piecewise H2D/K2/D2H pipeline;
+    force tiny pieces so a modest stream spans several of them."""
+    m = sz()
+    from paper_2605_01708_b200 import hostpipe
+    monkeypatch.setattr(hostpipe, "PIECE_ELEMS", 1 << 16)
+    n = (1 << 18) + 12345
+    words = O.exact_stream(0, n, 0.0123, 77, O.BF16_BOOK, O.BF16_ESC)
+    book = tuple(e for e, _ in O.BF16_BOOK)
+    cfg = m.CodecConfig(m.ElementFormat.BF16, chunk_size=1024, codebook=m.ExponentCodebook(
+        m.ElementFormat.BF16, book, 4, m.CodebookMode.TOPK_EXPLICIT))
+    if host_kind == "numpy":
+        src = words
+    else:
+        src = torch.from_numpy(words.copy())
+        if host_kind == "pinned":
+            src = src.pin_memory()
+    stream = m.RawTensorStream(m.ElementFormat.BF16, src)
+    assert hostpipe.pipelinable(cfg, n)
+    enc = m.encode(stream, cfg)
+    ref = O.encode(words, O.Params(0), book)
+    assert [b for _, b in enc.section_bytes()] == O.section_bytes(ref)
+    dec = m.decode(enc, cfg, enc.codebook)
+    out = dec.words.numpy() if isinstance(dec.words, torch.Tensor) else dec.words
+    assert np.array_equal(out, words)
+    # a corrupted host stream still raises with the reference's verdict
+    if host_kind == "numpy":
+        pos = enc.escape_positions.copy()
+        pos[3] = 1024
+        bad = m.EncodedStreams(enc.n_elements, enc.n_escapes, enc.packed_codes,
+                               enc.sign_mantissa, enc.chunk_counts, pos, enc.escape_values,
+                               enc.codebook)
+        with pytest.raises(m.CorruptionError) as exc:
+            m.decode(bad, cfg, enc.codebook)
+        sec = dict(ref, escape_positions=pos)
+        with pytest.raises(O.OracleCorruption) as oexc:
+            O.decode(sec, O.Params(0), book)
+        assert exc.value.chunk == oexc.value.chunk

@@ -36,7 +36,7 @@ def test_struct_layouts_match_header():
     import ctypes as C
     assert C.sizeof(N.SzParams) == 6 * 4 + 256 + 16
     assert C.sizeof(N.SzDecodeStatus) == 8 + 13 * 8 + 16
-    assert C.sizeof(N.SzEncoded) == 8 * 8
+    assert C.sizeof(N.SzEncoded) == 9 * 8
     assert C.sizeof(N.SzEncodedIn) == 5 * 8 + 3 * 8 + 8
 
 
