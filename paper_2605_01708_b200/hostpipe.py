@@ -160,7 +160,8 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
 
     codes_h = host_tensor(streams.packed_codes, torch.uint8)
     sm_h = host_tensor(streams.sign_mantissa, torch.uint8)
-    counts_h = host_tensor(counts_np.astype(np.uint32, copy=False), torch.uint32)
+    # small metadata: pinned so the H2D stream never blocks the host thread
+    counts_h = host_tensor(counts_np.astype(np.uint32, copy=False), torch.uint32).pin_memory()
     # ordinal offset of every piece = escapes in the chunks before it
     prefix = np.concatenate([[0], np.cumsum(counts_np.astype(np.int64))])
     out_h = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
@@ -220,6 +221,9 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     cur.wait_stream(st.d2h)
     cur.wait_stream(st.comp)
     raw = status.cpu().numpy()
-    if raw.any():
+    # verdict words only: flags + first_inv[] (counts_total / marks_total are
+    # informational and always set)
+    verdict_bytes = 8 + 8 * N.NUM_CHECKS
+    if raw[:, :verdict_bytes].any():
         return None
     return out_h
