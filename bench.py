@@ -299,12 +299,19 @@ def run_ours(args) -> None:
     dominant = "encode" if enc_launch_ms >= dec_launch_ms else "decode"
     dom_ms = max(enc_launch_ms, dec_launch_ms)
     achieved = alg_bytes / (dom_ms / 1e3) / 1e9
+    # DRAM traffic of the dominant kernel from the committed `ncu --set full`
+    # capture (profiles/ncu_traffic_<workload>_r*.json, bytes per element),
+    # scaled to this launch's element count.
     traffic = None
-    prof = ROOT / "profiles" / f"ncu_traffic_{wl['name']}.json"
-    if prof.exists():
+    wl_prof = "c3" if wl["name"] == "c3" else "c2"
+    profs = sorted((ROOT / "profiles").glob(f"ncu_traffic_{wl_prof}_r*.json"))
+    if profs:
         try:
-            traffic = json.loads(prof.read_text()).get(f"{dominant}_kernel_dram_bytes")
-        except Exception:
+            per_elem = json.loads(profs[-1].read_text())["dram_bytes_per_element"]
+            kname = "encode_tiles" if dominant == "encode" else "decode_persistent"
+            if kname in per_elem:
+                traffic = int(per_elem[kname] * n)
+        except (ValueError, KeyError):
             traffic = None
 
     value = world * raw * K / (tot_ms / 1e3) / 1e9
