@@ -273,3 +273,27 @@ def test_host_pipeline_matches_oracle(host_kind, monkeypatch):
         with pytest.raises(O.OracleCorruption) as oexc:
             O.decode(sec, O.Params(0), book)
         assert exc.value.chunk == oexc.value.chunk
+
+
+@pytest.mark.parametrize("rate", [0.0016, 0.0789, 0.5])
+def test_gpu_piece_codec_loopback(rate):
+    """The handoff's product binding (GpuPieceCodec) on one GPU: encode
+    pieces, copy the wire tensors as NCCL would, decode into place."""
+    m = sz()
+    from paper_2605_01708_b200.distributed import GpuPieceCodec
+    n, piece = 300_000, 1 << 16
+    words = O.exact_stream(0, n, rate, 3, O.BF16_BOOK, O.BF16_ESC)
+    book = m.ExponentCodebook(m.ElementFormat.BF16, tuple(e for e, _ in O.BF16_BOOK), 4,
+                              m.CodebookMode.TOPK_EXPLICIT)
+    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
+    tx, rx = GpuPieceCodec(cfg, book), GpuPieceCodec(cfg, book)
+    src = torch.from_numpy(words).cuda()
+    out = torch.empty_like(src)
+    for k, lo in enumerate(range(0, n, piece)):
+        sec = tx.encode(src[lo:lo + piece], k % 2)
+        dst = rx.empty_sections(sec.n, sec.m, k % 2)
+        for a, b in zip(dst.wire(), sec.wire()):
+            a.copy_(b)
+        rx.decode_into(dst, out[lo:lo + piece], k % 2)
+    rx.finish()
+    assert torch.equal(out, src)
