@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.staged[s], 1);
+      mbar_init(&S.staged[s], 32);  // every stager lane arrives
       mbar_init(&S.empty[s], kThreads);
     }
     fence_barrier_init();
@@ -549,6 +549,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       const uint64_t tile = S.meta[s];
       if (tile == ~0ull) break;
       const uint64_t s0 = tile * TILE, s1 = min(s0 + TILE, n);
+      // Direct happens-before with the decode warps' last use of this stage
+      // (already guaranteed through the producer's chain; free to re-check).
+      mbar_wait(&S.empty[s], ph ^ 1);
 #pragma unroll
       for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
       if constexpr (ABS) {
@@ -639,7 +642,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&S.staged[s]);
+      mbar_arrive(&S.staged[s]);
     }
     return;
   }

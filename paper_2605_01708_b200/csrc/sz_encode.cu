@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     }
     for (int q = 0; q < kEncScanSlots; ++q) {
       mbar_init(&S.computed[q], kEncDense);
-      mbar_init(&S.scan_empty[q], 1);
+      mbar_init(&S.scan_empty[q], 32);  // every writer lane arrives
       S.esc_n[q] = 0;
     }
     fence_barrier_init();
@@ -285,9 +285,12 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     long long t_wait = 0, t_work = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
-      const uint32_t q = it % kEncScanSlots;
+      const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
       const long long c0 = SZ_CLOCK();
       mbar_wait(&S.full[s], sph);
+      // direct ordering after the writer's release of this scan slot (also
+      // implied through the producer; re-checked at no cost)
+      mbar_wait(&S.scan_empty[q], qph ^ 1);
       const long long c1 = SZ_CLOCK();
       t_wait += c1 - c0;
       const uint64_t tile = S.meta[q];
@@ -448,10 +451,9 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     }
     // (tiles with more than kEscCap escapes are re-derived by escape_gather)
     __syncwarp();
-    if (lane == 0) {
-      S.esc_n[q] = 0;
-      mbar_arrive(&S.scan_empty[q]);
-    }
+    if (lane == 0) S.esc_n[q] = 0;
+    __syncwarp();
+    mbar_arrive(&S.scan_empty[q]);
     t_work += SZ_CLOCK() - c1;
   }
   if (a.dbg && lane == 0) {

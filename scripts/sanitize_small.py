@@ -1,0 +1,28 @@
+"""Small encode/decode runs across formats/modes for compute-sanitizer."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2605_01708_b200 as sz  # noqa: E402
+from oracle import sz_oracle as O  # noqa: E402
+
+for fmt_id, fmt, bk, esc in ((0, sz.ElementFormat.BF16, O.BF16_BOOK, O.BF16_ESC),
+                             (1, sz.ElementFormat.FP8_E5M2, O.E5M2_BOOK, O.E5M2_ESC)):
+    for rate, chunk, mode, pos in ((0.0016, 1024, "explicit", "chunk"), (0.3, 256, "explicit", "chunk"),
+                                   (0.01, 3000, "explicit", "chunk"), (0.01, 1024, "explicit", "abs32"),
+                                   (0.01, 1024, "sentinel", "chunk")):
+        n = 200_003
+        words = O.exact_stream(fmt_id, n, rate, 5, bk, esc)
+        m = sz.CodebookMode.from_name(mode)
+        book = tuple(e for e, _ in bk)[: (15 if mode == "sentinel" else 16)]
+        cfg = sz.CodecConfig(fmt, 4, m, chunk, pos, sz.ExponentCodebook(fmt, book, 4, m))
+        st = sz.RawTensorStream(fmt, torch.from_numpy(words).cuda())
+        enc = sz.encode(st, cfg)
+        dec = sz.decode(enc, cfg, enc.codebook)
+        assert sz.compare_streams(st, dec).ok
+        sz.build_histogram(st)
+torch.cuda.synchronize()
+print("sanitize ok")
