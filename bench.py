@@ -208,6 +208,16 @@ def run_ours(args) -> None:
 
     # ---- calibration: K1 histogram per rank, NCCL all-reduce = merge_stats
     counts = build_histogram_device(words, fmt)
+    # calibration-histogram throughput (K1), reported beside the codec numbers
+    for _ in range(2):
+        build_histogram_device(words, fmt)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record()
+    for _ in range(5):
+        build_histogram_device(words, fmt)
+    h1.record()
+    torch.cuda.synchronize()
+    hist_gbs = 5 * n * fmt.word_nbytes / (h0.elapsed_time(h1) / 1e3) / 1e9
     if world > 1:
         dist.all_reduce(counts, op=dist.ReduceOp.SUM)
     stats = sz.CalibrationStats(fmt, counts.cpu().numpy(), n * world)
@@ -340,7 +350,8 @@ def run_ours(args) -> None:
         "e2e": {"value": round(world * raw * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                 "api": "paper_2605_01708_b200.encode/decode on pinned host words"},
-        "gpu_launches": K * (3 + (1 if fmt.exp_bits != 8 else 0)),
+        "gpu_launches": K * (4 + (1 if fmt.exp_bits != 8 else 0)),
+        "calibration_histogram_gbs": round(hist_gbs, 1),
         "clocks": clocks,
     }
 

@@ -462,7 +462,6 @@ struct DecSmem {
   alignas(16) uint8_t vals[STAGES][TILE];
   uint32_t bitmap[STAGES][TILE / 32];
   uint64_t off[kDecHelpers][kDecOffStage + 1];
-  uint32_t lut2[256];
   uint64_t meta[STAGES];
   uint64_t full[STAGES];
   uint64_t staged[STAGES];
@@ -491,11 +490,15 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
+  // Pair LUT in static shared memory, 1 KiB aligned: the address of entry i
+  // is base | (i << 2), formed with one SHF + one LOP3 (no base add).
+  __shared__ __align__(1024) uint32_t s_lut2[256];
   for (int i = tid; i < LUT2; i += kDecThreads) {
     const uint32_t c0 = i & kCodeMask, c1 = (i >> CB) & kCodeMask;
     const uint32_t bad = (c0 >= p.n_entries) | ((c1 >= p.n_entries) << 1);
-    S.lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
+    s_lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
+  const uint32_t lut2_base = smem_addr(s_lut2);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
@@ -700,13 +703,19 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       for (int g = 0; g < G; ++g) {
         uint32_t l0, l1;
         if constexpr (CB == 4) {
-          const uint32_t cb16 = group_bits<16>(cw, g);
-          l0 = S.lut2[cb16 & 0xFF];
-          l1 = S.lut2[cb16 >> 8];
+          // code bytes 2g, 2g+1 of the slot: word g/2, bit offset 16*(g&1)
+          const uint32_t w = cw[g >> 1];
+          if ((g & 1) == 0) {
+            l0 = lds_u32(lut2_base | ((w << 2) & 0x3FCu));
+            l1 = lds_u32(lut2_base | ((w >> 6) & 0x3FCu));
+          } else {
+            l0 = lds_u32(lut2_base | ((w >> 14) & 0x3FCu));
+            l1 = lds_u32(lut2_base | ((w >> 22) & 0x3FCu));
+          }
         } else {
           const uint32_t cb12 = group_bits<12>(cw, g);
-          l0 = S.lut2[cb12 & 0x3F];
-          l1 = S.lut2[cb12 >> 6];
+          l0 = lds_u32(lut2_base | ((cb12 << 2) & 0xFCu));
+          l1 = lds_u32(lut2_base | ((cb12 >> 4) & 0xFCu));
         }
         eg[g] = __byte_perm(l0, l1, 0x5410);
         if (check_range) bad |= (((l0 >> 16) & 3) | (((l1 >> 16) & 3) << 2)) << (4 * g);

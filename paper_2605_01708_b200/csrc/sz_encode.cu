@@ -83,7 +83,6 @@ struct EncSmem {
   uint64_t in_empty[kEncInStages];   // dense -> producer
   uint64_t computed[kEncScanSlots];  // dense -> writer
   uint64_t scan_empty[kEncScanSlots];// writer -> producer
-  uint8_t lut[256];
 };
 
 template <int FMT>
@@ -104,9 +103,18 @@ __device__ __forceinline__ void split_group(const uint32_t (&x)[8], int g, uint3
   }
 }
 
+// Four marked-LUT lookups.  Each byte index is extracted with one PRMT and
+// the LUT lives in static shared memory, so every lookup is PRMT + LDS with
+// an immediate base (no shift/mask/base-add sequence).
+// `lut` is 256-byte aligned, so the shared address of entry e is the LUT's
+// address with its low byte replaced by e: one PRMT builds it (byte k of e4
+// into byte 0, bytes 1-3 from the base) — no shift / mask / add.
 __device__ __forceinline__ uint32_t lut4(const uint8_t* lut, uint32_t e4) {
-  const uint32_t m0 = lut[e4 & 0xFF], m1 = lut[(e4 >> 8) & 0xFF];
-  const uint32_t m2 = lut[(e4 >> 16) & 0xFF], m3 = lut[e4 >> 24];
+  const uint32_t base = smem_addr(lut);
+  const uint32_t m0 = lds_u8(__byte_perm(e4, base, 0x7650));
+  const uint32_t m1 = lds_u8(__byte_perm(e4, base, 0x7651));
+  const uint32_t m2 = lds_u8(__byte_perm(e4, base, 0x7652));
+  const uint32_t m3 = lds_u8(__byte_perm(e4, base, 0x7653));
   return __byte_perm(__byte_perm(m0, m1, 0x0040), __byte_perm(m2, m3, 0x0040), 0x5410);
 }
 
@@ -219,7 +227,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
-  for (int i = tid; i < 256; i += kEncThreads) S.lut[i] = p.enc_lut[i];
+  __shared__ __align__(256) uint8_t s_lut[256];  // 256-aligned: PRMT-built addresses in lut4
+  for (int i = tid; i < 256; i += kEncThreads) s_lut[i] = p.enc_lut[i];
   if (blockIdx.x == 0 && tid == 0) *a.base_snapshot = a.escape_base ? *a.escape_base : 0;
   if (tid == 0) {
     for (int s = 0; s < kEncInStages; ++s) {
@@ -305,18 +314,30 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       uint8_t* const stile = a.sm + tile_e0 * SMB / 8;
       uint32_t x[kEncItems][8];
       int nv[kEncItems];
+      if (!tail_tile) {
+        // steady state: every slot is full and in the TMA stage
 #pragma unroll
-      for (int i = 0; i < kEncItems; ++i) {
-        const int slot = i * kEncDense + tid;
-        const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
-        nv[i] = !tail_tile || e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
-        if (nv[i] == EPV) {
-          const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + slot * 32);
+        for (int i = 0; i < kEncItems; ++i) {
+          const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + (i * kEncDense + tid) * 32);
           const uint4 v0 = src[0], v1 = src[1];
           x[i][0] = v0.x; x[i][1] = v0.y; x[i][2] = v0.z; x[i][3] = v0.w;
           x[i][4] = v1.x; x[i][5] = v1.y; x[i][6] = v1.z; x[i][7] = v1.w;
-        } else {
-          ld_bytes_clipped<32>(a.words, e0 * WB, x[i], nv[i] > 0 ? n * WB : 0);
+          nv[i] = EPV;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kEncItems; ++i) {
+          const int slot = i * kEncDense + tid;
+          const uint64_t e0 = tile_e0 + static_cast<uint64_t>(slot) * EPV;
+          nv[i] = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
+          if (nv[i] == EPV) {
+            const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + slot * 32);
+            const uint4 v0 = src[0], v1 = src[1];
+            x[i][0] = v0.x; x[i][1] = v0.y; x[i][2] = v0.z; x[i][3] = v0.w;
+            x[i][4] = v1.x; x[i][5] = v1.y; x[i][6] = v1.z; x[i][7] = v1.w;
+          } else {
+            ld_bytes_clipped<32>(a.words, e0 * WB, x[i], nv[i] > 0 ? n * WB : 0);
+          }
         }
       }
       mbar_arrive(&S.in_empty[s]);  // input stage free: the producer may refill it
@@ -325,10 +346,10 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         const int slot = i * kEncDense + tid;
         uint32_t fm;
         if (!tail_tile) {
-          fm = encode_slot<FMT, CB, false>(x[i], S.lut, EPV, ctile + slot * CBYTES,
+          fm = encode_slot<FMT, CB, false>(x[i], s_lut, EPV, ctile + slot * CBYTES,
                                            stile + slot * SBYTES, a, 0);
         } else {
-          fm = encode_slot<FMT, CB, true>(x[i], S.lut, nv[i], ctile + slot * CBYTES,
+          fm = encode_slot<FMT, CB, true>(x[i], s_lut, nv[i], ctile + slot * CBYTES,
                                           stile + slot * SBYTES, a,
                                           tile_e0 + static_cast<uint64_t>(slot) * EPV);
         }
