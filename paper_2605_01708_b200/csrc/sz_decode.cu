@@ -454,7 +454,7 @@ constexpr int kDecOffStage = 256;                       // staged chunk offsets 
 
 template <int FMT>
 struct DecSmem {
-  static constexpr int STAGES = FMT == SZ_BF16 ? 4 : 3;
+  static constexpr int STAGES = FMT == SZ_BF16 ? 5 : 3;
   static constexpr int EPV = kEpv<FMT>;
   static constexpr int TILE = kDecSlots * EPV;
   alignas(128) uint8_t codes[STAGES][TILE / 2];              // <= 4-bit codes
@@ -465,6 +465,7 @@ struct DecSmem {
   uint64_t meta[STAGES];
   uint64_t full[STAGES];
   uint64_t staged[STAGES];
+  uint64_t claimed[STAGES];   // producer -> stagers: tile id written (before TMA)
   uint64_t empty[STAGES];
 };
 
@@ -503,6 +504,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.staged[s], 32);  // every stager lane arrives
+      mbar_init(&S.claimed[s], 1);
       mbar_init(&S.empty[s], kThreads);
     }
     fence_barrier_init();
@@ -522,11 +524,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             const uint32_t sk = (it + k) % kStages, pk = ((it + k) / kStages) & 1;
             if (k) mbar_wait(&S.empty[sk], pk ^ 1);
             S.meta[sk] = ~0ull;
+            mbar_arrive(&S.claimed[sk]);
             mbar_arrive(&S.full[sk]);
           }
           break;
         }
         S.meta[s] = tile;
+        // stagers start on the tile's escapes while its planes are in flight
+        mbar_arrive(&S.claimed[s]);
         const uint64_t e0 = tile * TILE;
         const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
         const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     uint64_t* soff = S.off[h];
     for (uint32_t it = h;; it += kDecHelpers) {
       const uint32_t s = it % kStages, ph = (it / kStages) & 1;
-      mbar_wait(&S.full[s], ph);
+      mbar_wait(&S.claimed[s], ph);
       const uint64_t tile = S.meta[s];
       if (tile == ~0ull) break;
       const uint64_t s0 = tile * TILE, s1 = min(s0 + TILE, n);
@@ -730,22 +735,26 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       uint32_t bm;
       if constexpr (EPV == 32) bm = S.bitmap[s][slot];
       else bm = (S.bitmap[s][slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
-      if (bm) {
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int j = 4 * g + b;
-            if ((bm >> j) & 1u) {
-              uint32_t code;
-              if constexpr (CB == 4) code = (cw[j >> 3] >> (4 * (j & 7))) & 0xF;
-              else code = (group_bits<12>(cw, g) >> (3 * b)) & 7;
-              if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-              const uint32_t v = S.vals[s][slot * EPV + j];
-              eg[g] = (eg[g] & ~(0xFFu << (8 * b))) | (v << (8 * b));
-            }
-          }
+      // rare: overwrite escaped exponents (compact loop over set bits; the
+      // register arrays are indexed through selects, never dynamically)
+      while (bm) {
+        const int j = __ffs(bm) - 1;
+        bm &= bm - 1;
+        uint32_t code;
+        if constexpr (CB == 4) {
+          code = (pick<CWORDS>(cw, j >> 3) >> (4 * (j & 7))) & 0xF;
+        } else {
+          const int bit = 3 * j;
+          const uint64_t lo = pick<CWORDS>(cw, bit >> 5);
+          const uint64_t hi = pick<CWORDS>(cw, (bit >> 5) + 1);
+          code = static_cast<uint32_t>(((hi << 32) | lo) >> (bit & 31)) & 7;
         }
+        if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+        const uint32_t v = S.vals[s][slot * EPV + j];
+        const int g = j >> 2, sh = 8 * (j & 3);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg)
+          if (gg == g) eg[gg] = (eg[gg] & ~(0xFFu << sh)) | (v << sh);
       }
       uint32_t ow[8];
 #pragma unroll

@@ -356,17 +356,17 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         S.fmask[q][slot] = fm;
         if (fm) {  // rare: append (element, raw exponent) records for the writer
           uint32_t r = atomicAdd(&S.esc_n[q], static_cast<uint32_t>(__popc(fm)));
-#pragma unroll
-          for (int j = 0; j < EPV; ++j) {
-            if ((fm >> j) & 1u) {
-              uint32_t word;
-              if constexpr (WB == 2) word = (x[i][j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
-              else word = (x[i][j >> 2] >> (8 * (j & 3))) & 0xFFu;
-              if (r < kEscCap)
-                S.esc_rec[q][r] = static_cast<uint32_t>(slot * EPV + j) |
-                                  (raw_exponent<FMT>(word) << 16);
-              ++r;
-            }
+          uint32_t f = fm;
+          while (f) {  // compact loop; x[] read through selects (no local memory)
+            const int j = __ffs(f) - 1;
+            f &= f - 1;
+            uint32_t word;
+            if constexpr (WB == 2) word = (pick<8>(x[i], j >> 1) >> (16 * (j & 1))) & 0xFFFFu;
+            else word = (pick<8>(x[i], j >> 2) >> (8 * (j & 3))) & 0xFFu;
+            if (r < kEscCap)
+              S.esc_rec[q][r] = static_cast<uint32_t>(slot * EPV + j) |
+                                (raw_exponent<FMT>(word) << 16);
+            ++r;
           }
         }
       }
