@@ -39,7 +39,9 @@ struct OffsetsArgs {
   sz_decode_status* status;
 };
 
-constexpr int kOffItems = 16;  // counts per thread
+// counts per thread: 64 -> 16384 chunks per CTA, so the look-back chain of
+// this latency-bound scan is short (2^31 words at c=1024 -> 128 CTAs)
+constexpr int kOffItems = 64;
 
 __global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) {
   __shared__ uint64_t warp_tot[kWarps];
@@ -52,11 +54,19 @@ __global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) 
   const uint64_t base = (tile * kThreads + tid) * kOffItems;
   uint32_t v[kOffItems];
   uint64_t sum = 0;
+  if (base + kOffItems <= a.n_counts && !(reinterpret_cast<uintptr_t>(a.counts) & 15)) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.counts + base);
 #pragma unroll
-  for (int j = 0; j < kOffItems; ++j) {
-    v[j] = base + j < a.n_counts ? a.counts[base + j] : 0u;
-    sum += v[j];
+    for (int j = 0; j < kOffItems / 4; ++j) {
+      const uint4 q = __ldg(src + j);
+      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kOffItems; ++j) v[j] = base + j < a.n_counts ? a.counts[base + j] : 0u;
   }
+#pragma unroll
+  for (int j = 0; j < kOffItems; ++j) sum += v[j];
   // block exclusive scan of per-thread sums (u64: corrupted counts may be huge)
   uint64_t incl = sum;
 #pragma unroll

@@ -505,7 +505,9 @@ struct GatherArgs {
   uint64_t* escape_base;          // append mode: advanced by this call's M
 };
 
-constexpr int kGatherTiles = 32;  // tiles per CTA (one warp handles 4)
+// Tiles per CTA: 256 (8 per lane in the scan) keeps the look-back chain
+// short — K2b is latency-bound, so fewer, fatter CTAs win.
+constexpr int kGatherTiles = 256;
 
 template <int FMT, int POSB>
 __global__ void __launch_bounds__(kThreads)
@@ -523,9 +525,17 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t group = s_group;
   const uint64_t t0 = group * kGatherTiles;
   if (warp == 0) {
-    const uint64_t t = t0 + lane;
-    const uint32_t c = t < a.num_tiles ? a.tile_esc[t] : 0u;
-    uint64_t incl = c;
+    // each lane owns kTilesPerLane consecutive tiles of the group
+    constexpr int kTilesPerLane = kGatherTiles / 32;
+    uint32_t c[kTilesPerLane];
+    uint64_t lsum = 0;
+#pragma unroll
+    for (int j = 0; j < kTilesPerLane; ++j) {
+      const uint64_t t = t0 + lane * kTilesPerLane + j;
+      c[j] = t < a.num_tiles ? a.tile_esc[t] : 0u;
+      lsum += c[j];
+    }
+    uint64_t incl = lsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
@@ -534,8 +544,13 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t agg = __shfl_sync(0xffffffffu, incl, 31);
     const uint64_t ex = lookback_warp(a.states, group, agg);
     const uint64_t base = *a.base_snapshot;
-    tpref[lane] = base + ex + incl - c;
-    tcnt[lane] = c;
+    uint64_t run = base + ex + incl - lsum;
+#pragma unroll
+    for (int j = 0; j < kTilesPerLane; ++j) {
+      tpref[lane * kTilesPerLane + j] = run;
+      tcnt[lane * kTilesPerLane + j] = c[j];
+      run += c[j];
+    }
     if (lane == 0 && group == a.num_groups - 1) {
       *a.n_escapes = ex + agg;
       if (a.escape_base) *a.escape_base = base + ex + agg;
