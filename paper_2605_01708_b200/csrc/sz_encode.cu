@@ -118,6 +118,55 @@ __device__ __forceinline__ uint32_t lut4(const uint8_t* lut, uint32_t e4) {
   return __byte_perm(__byte_perm(m0, m1, 0x0040), __byte_perm(m2, m3, 0x0040), 0x5410);
 }
 
+// ---------------------------------------------------------------- T4 tables
+// Lane tables for 4-bit codes (the north-star configuration):
+//   t4[k][e] = code(e) << 4k  |  escape(e) << (16 + k)
+// so the OR of the four lane-k lookups of a 4-element group is that group's
+// packed nibble group (bits 0-15, element 0 in the low nibble — the order of
+// formats.py:180-183) with its escape flags in bits 16-19.  One lookup per
+// element replaces lookup + byte merge + nibble pack + flag extraction.
+// E5M2: 32 entries per lane, lanes 128 B apart; the entry address is the
+// exponent field itself (x & 0x7C = 4e) spliced into the table base by one
+// PRMT.  BF16: 256 entries per lane, lanes 1 KB apart; 4e = (x >> 5) & 0x3FC.
+template <int FMT> constexpr int kT4Entries = FMT == SZ_BF16 ? 256 : 32;
+template <int FMT, int CB> constexpr bool kUseT4 = CB == 4 && FMT != SZ_E4M3;
+
+template <int OFF>
+__device__ __forceinline__ uint32_t lds_u32_off(uint32_t saddr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(saddr), "n"(OFF));
+  return v;
+}
+
+// Codes + flags of group g (elements 4g..4g+3) of a 32-byte slot.
+template <int FMT>
+__device__ __forceinline__ uint32_t t4_group(const uint32_t (&x)[8], int g, uint32_t base) {
+  if constexpr (FMT == SZ_E5M2) {
+    const uint32_t f = x[g] & 0x7C7C7C7Cu;  // byte k = 4 * exponent of element k
+    const uint32_t t0 = lds_u32_off<0>(__byte_perm(f, base, 0x7650));
+    const uint32_t t1 = lds_u32_off<128>(__byte_perm(f, base, 0x7651));
+    const uint32_t t2 = lds_u32_off<256>(__byte_perm(f, base, 0x7652));
+    const uint32_t t3 = lds_u32_off<384>(__byte_perm(f, base, 0x7653));
+    return t0 | t1 | t2 | t3;
+  } else {
+    const uint32_t f0 = (x[2 * g] >> 5) & 0x03FC03FCu;      // 4e of elements 4g, 4g+1
+    const uint32_t f1 = (x[2 * g + 1] >> 5) & 0x03FC03FCu;  // 4e of elements 4g+2, 4g+3
+    const uint32_t t0 = lds_u32_off<0>(base + (f0 & 0xFFFFu));
+    const uint32_t t1 = lds_u32_off<1024>(base + (f0 >> 16));
+    const uint32_t t2 = lds_u32_off<2048>(base + (f1 & 0xFFFFu));
+    const uint32_t t3 = lds_u32_off<3072>(base + (f1 >> 16));
+    return t0 | t1 | t2 | t3;
+  }
+}
+
+// E5M2 sign|mantissa 3-bit symbols of group g as a 12-bit little-endian group
+// (formats.py:184-189 on a = sign<<2 | mantissa, formats.py:123-125): the
+// six bits of elements (0,1) gather at bits 0-5 and of (2,3) at bits 16-21.
+__device__ __forceinline__ uint32_t e5m2_sm12(uint32_t x) {
+  const uint32_t u = (x & 0x00030003u) | ((x >> 5) & 0x001C001Cu) | ((x >> 10) & 0x00200020u);
+  return (u | (u >> 10)) & 0xFFFu;
+}
+
 template <int FMT>
 __device__ __forceinline__ uint32_t raw_exponent(uint32_t word) {
   if constexpr (FMT == SZ_BF16) return (word >> 7) & 0xFF;
@@ -139,6 +188,51 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
   constexpr int SBYTES = EPV * SMB / 8;
   constexpr int CWORDS = (CBYTES + 3) / 4;
   constexpr int SWORDS = (SBYTES + 3) / 4;
+  if constexpr (kUseT4<FMT, CB>) {
+    const uint32_t base = smem_addr(lut);  // the T4 tables (see t4_group)
+    uint32_t r[G];
+    uint32_t any = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      r[g] = t4_group<FMT>(x, g, base);
+      if (TAIL && nv < EPV) {  // tail slot: no codes or flags beyond N (x is 0 there)
+        const int v = min(max(nv - 4 * g, 0), 4);
+        r[g] &= v >= 4 ? 0xFFFFFFFFu : (((1u << (4 * v)) - 1u) | (((1u << v) - 1u) << 16));
+      }
+      any |= r[g];
+    }
+    uint32_t fm = 0;
+    if (any & 0x000F0000u) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) fm |= ((r[g] >> 16) & 0xFu) << (4 * g);
+    }
+    uint32_t cw[CWORDS], sw[SWORDS];
+#pragma unroll
+    for (int i = 0; i < CWORDS; ++i) cw[i] = __byte_perm(r[2 * i], r[2 * i + 1], 0x5410);
+    if constexpr (FMT == SZ_BF16) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const uint32_t lo4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x6420);
+        const uint32_t hi4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x7531);
+        sw[g] = (hi4 & 0x80808080u) | (lo4 & 0x7F7F7F7Fu);
+      }
+    } else {
+      uint32_t p[4];  // 24-bit SM groups of 8 elements
+#pragma unroll
+      for (int i = 0; i < 4; ++i) p[i] = e5m2_sm12(x[2 * i]) | (e5m2_sm12(x[2 * i + 1]) << 12);
+      sw[0] = p[0] | (p[1] << 24);
+      sw[1] = (p[1] >> 8) | (p[2] << 16);
+      sw[2] = (p[2] >> 16) | (p[3] << 8);
+    }
+    if (!TAIL || nv == EPV) {
+      st_packed<CBYTES>(cdst, cw);
+      st_packed<SBYTES>(sdst, sw);
+    } else if (nv > 0) {
+      st_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, a.codes_len);
+      st_bytes_clipped<SBYTES>(a.sm, e0 * SMB / 8, sw, a.sm_len);
+    }
+    return fm;
+  }
   uint32_t mk[G], ag[G];
   uint32_t any = 0;
 #pragma unroll
@@ -227,8 +321,21 @@ __global__ void __launch_bounds__(kEncThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
-  __shared__ __align__(256) uint8_t s_lut[256];  // 256-aligned: PRMT-built addresses in lut4
-  for (int i = tid; i < 256; i += kEncThreads) s_lut[i] = p.enc_lut[i];
+  // 4-bit codes: T4 lane tables (t4_group); otherwise the 256-byte marked LUT
+  // (256-aligned: PRMT-built addresses in lut4).
+  __shared__ __align__(1024) uint32_t s_tab[kUseT4<FMT, CB> ? 4 * kT4Entries<FMT> : 64];
+  const uint8_t* s_lut = reinterpret_cast<const uint8_t*>(s_tab);
+  if constexpr (kUseT4<FMT, CB>) {
+    constexpr int TE = kT4Entries<FMT>;
+    for (int i = tid; i < 4 * TE; i += kEncThreads) {
+      const int k = i / TE, e = i % TE;
+      const uint32_t m = p.enc_lut[e];
+      s_tab[i] = ((m & 0xFu) << (4 * k)) | (((m >> 4) & 1u) << (16 + k));
+    }
+  } else {
+    for (int i = tid; i < 256; i += kEncThreads)
+      reinterpret_cast<uint8_t*>(s_tab)[i] = p.enc_lut[i];
+  }
   if (blockIdx.x == 0 && tid == 0) *a.base_snapshot = a.escape_base ? *a.escape_base : 0;
   if (tid == 0) {
     for (int s = 0; s < kEncInStages; ++s) {
