@@ -124,6 +124,13 @@ __device__ __forceinline__ uint32_t pick(const uint32_t* w, int k) {
 }
 
 // -------------------------------------------------------- bit shuffling
+// (a & mask) | (b & ~mask) as one LOP3 (ptxas does not always fuse the
+// two-constant form).
+__device__ __forceinline__ uint32_t bitselect(uint32_t a, uint32_t b, uint32_t mask) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(mask));
+  return d;
+}
 // Four bytes, each < 16, to one 16-bit nibble group (element 0 low nibble) —
 // the nibble order of formats.py:180-183.
 __device__ __forceinline__ uint32_t pack_nib4(uint32_t b4) {

@@ -165,6 +165,17 @@ __device__ __forceinline__ void rebuild_group(uint32_t e4, uint32_t a4, uint32_t
   }
 }
 
+// E5M2 12-bit sign|mantissa group (four 3-bit symbols a = s<<2 | m,
+// formats.py:123-125,184-189) -> the sign and mantissa bits of four E5M2
+// bytes (bit 7 and bits 0-1).  The two spreads and the final a*33 (copies
+// bit 2 of each symbol to bit 7) are left shifts the compiler can issue on
+// the FMA pipe, next to the ALU-bound lookups.
+__device__ __forceinline__ uint32_t e5m2_sm_bytes(uint32_t v12) {
+  const uint32_t u = (v12 | (v12 << 10)) & 0x003F003Fu;  // symbols (0,1) | (2,3) << 16
+  const uint32_t t = (u | (u << 5)) & 0x07070707u;       // one symbol per byte
+  return (t * 33u) & 0x83838383u;
+}
+
 // Warp-cooperative lower_bound over sorted u32 positions [0, m) (abs32 mode).
 __device__ uint64_t warp_lower_bound(const uint32_t* pos, uint64_t m, uint64_t target) {
   const int lane = threadIdx.x & 31;
@@ -510,6 +521,20 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     s_lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
   const uint32_t lut2_base = smem_addr(s_lut2);
+  // E5M2 with 4-bit codes: two pair tables indexed by a code byte (elements
+  // 2i, 2i+1) whose entries hold both exponents already at their E5M2 bit
+  // positions (bits 2-6 of bytes 0/1, resp. 2/3) — reconstruct
+  // (formats.py:136-155) becomes lookup | lookup | sign-mantissa bits.
+  constexpr bool kE5Fast = FMT == SZ_E5M2 && CB == 4;
+  __shared__ __align__(1024) uint32_t s_e5[kE5Fast ? 512 : 1];
+  const uint8_t* e5tab = reinterpret_cast<const uint8_t*>(s_e5);
+  if constexpr (kE5Fast) {
+    for (int i = tid; i < 512; i += kDecThreads) {
+      const uint32_t b = i & 255, sh = i >= 256 ? 16 : 0;
+      s_e5[i] = ((static_cast<uint32_t>(p.dec_lut[b & 15]) << 2) |
+                 (static_cast<uint32_t>(p.dec_lut[b >> 4]) << 10)) << sh;
+    }
+  }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&S.full[s], 1);
@@ -711,6 +736,48 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       } else {
         ld_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, a.codes_len);
         ld_bytes_clipped<SBYTES>(a.sm, e0 * SMB / 8, sw, a.sm_len);
+      }
+      if constexpr (kE5Fast) {
+        // E5M2, 4-bit codes: placed-exponent pair tables + SWAR sign|mantissa
+        uint32_t ow[8];
+        uint32_t bad = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t w = cw[g >> 1];
+          const uint32_t blo = (g & 1) ? ((w >> 14) & 0x3FCu) : ((w << 2) & 0x3FCu);
+          const uint32_t bhi = (g & 1) ? ((w >> 22) & 0x3FCu) : ((w >> 6) & 0x3FCu);
+          const uint32_t ex = *reinterpret_cast<const uint32_t*>(e5tab + blo) |
+                              *reinterpret_cast<const uint32_t*>(e5tab + 1024 + bhi);
+          ow[g] = ex | e5m2_sm_bytes(group_bits<12>(sw, g));
+        }
+        if (check_range) {  // codebook < 16 entries: flag codes past its end
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t w = cw[g >> 1] >> (16 * (g & 1));
+            const uint32_t l0 = lds_u32(lut2_base | ((w << 2) & 0x3FCu));
+            const uint32_t l1 = lds_u32(lut2_base | ((w >> 6) & 0x3FCu));
+            bad |= (((l0 >> 16) & 3) | (((l1 >> 16) & 3) << 2)) << (4 * g);
+          }
+        }
+        if (bad) {
+          if (nv < 32) bad &= (1u << nv) - 1u;
+          if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
+        }
+        uint32_t bm = S.bitmap[s][slot];
+        while (bm) {  // rare: overwrite escaped exponent fields (bits 2-6 of the byte)
+          const int j = __ffs(bm) - 1;
+          bm &= bm - 1;
+          const uint32_t code = (pick<CWORDS>(cw, j >> 3) >> (4 * (j & 7))) & 0xF;
+          if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+          const uint32_t v = S.vals[s][slot * EPV + j];
+          const int g = j >> 2, sh = 8 * (j & 3);
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg)
+            if (gg == g) ow[gg] = (ow[gg] & ~(0x7Cu << sh)) | (v << (sh + 2));
+        }
+        if (nv == EPV) st256(a.out + e0 * WB, ow);
+        else st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
+        continue;
       }
       uint32_t eg[G], ag[G];
       uint32_t bad = 0;

@@ -214,7 +214,7 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
       for (int g = 0; g < G; ++g) {
         const uint32_t lo4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x6420);
         const uint32_t hi4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x7531);
-        sw[g] = (hi4 & 0x80808080u) | (lo4 & 0x7F7F7F7Fu);
+        sw[g] = bitselect(hi4, lo4, 0x80808080u);
       }
     } else {
       uint32_t p[4];  // 24-bit SM groups of 8 elements
@@ -615,6 +615,8 @@ struct GatherArgs {
 // Tiles per CTA: 256 (8 per lane in the scan) keeps the look-back chain
 // short — K2b is latency-bound, so fewer, fatter CTAs win.
 constexpr int kGatherTiles = 256;
+static_assert(kGatherTiles == 256, "escape_gather's search does exactly 8 halvings");
+constexpr int kGatherUnroll = 4;
 
 template <int FMT, int POSB>
 __global__ void __launch_bounds__(kThreads)
@@ -670,24 +672,42 @@ __global__ void __launch_bounds__(kThreads)
   {
     const uint64_t g_base = tpref[0];
     const uint64_t g_total = tpref[kGatherTiles - 1] + tcnt[kGatherTiles - 1] - g_base;
-    for (uint64_t r = tid; r < g_total; r += kThreads) {
-      const uint64_t o = g_base + r;
-      int lo = 0, hi = kGatherTiles;  // last k with tpref[k] <= o
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (tpref[mid] <= o) lo = mid; else hi = mid;
+    // kGatherUnroll records per thread per round: all loads are issued before
+    // any store, so the round costs one memory latency, not kGatherUnroll.
+    constexpr int U = kGatherUnroll;
+    for (uint64_t r0 = tid; r0 < g_total; r0 += kThreads * U) {
+      uint64_t src[U], dst[U];
+      uint32_t val[U], pos[U];
+      bool live[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t o = g_base + r0 + u * kThreads;
+        int lo = 0, hi = kGatherTiles;  // last k with tpref[k] <= o
+#pragma unroll
+        for (int step = 0; step < 8; ++step) {  // log2(kGatherTiles) halvings
+          const int mid = (lo + hi) >> 1;
+          if (tpref[mid] <= o) lo = mid; else hi = mid;
+        }
+        live[u] = r0 + u * kThreads < g_total && tcnt[lo] <= kEscCap && o < a.capacity;
+        src[u] = (t0 + lo) * kEscCap + (o - tpref[lo]);
+        dst[u] = o;
       }
-      const uint32_t c = tcnt[lo];
-      if (c > kEscCap || o >= a.capacity) continue;
-      const uint64_t tile = t0 + lo;
-      const uint64_t rr = o - tpref[lo];
-      a.values[o] = a.scr_val[tile * kEscCap + rr];
-      const uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
-      if constexpr (POSB == 1) a.positions[o] = spos[rr];
-      else if constexpr (POSB == 2)
-        reinterpret_cast<uint16_t*>(a.positions)[o] = reinterpret_cast<const uint16_t*>(spos)[rr];
-      else if constexpr (POSB == 4)
-        reinterpret_cast<uint32_t*>(a.positions)[o] = reinterpret_cast<const uint32_t*>(spos)[rr];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!live[u]) continue;
+        val[u] = __ldg(a.scr_val + src[u]);
+        if constexpr (POSB == 1) pos[u] = __ldg(a.scr_pos + src[u]);
+        else if constexpr (POSB == 2) pos[u] = __ldg(reinterpret_cast<const uint16_t*>(a.scr_pos) + src[u]);
+        else if constexpr (POSB == 4) pos[u] = __ldg(reinterpret_cast<const uint32_t*>(a.scr_pos) + src[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!live[u]) continue;
+        a.values[dst[u]] = static_cast<uint8_t>(val[u]);
+        if constexpr (POSB == 1) a.positions[dst[u]] = static_cast<uint8_t>(pos[u]);
+        else if constexpr (POSB == 2) reinterpret_cast<uint16_t*>(a.positions)[dst[u]] = static_cast<uint16_t>(pos[u]);
+        else if constexpr (POSB == 4) reinterpret_cast<uint32_t*>(a.positions)[dst[u]] = pos[u];
+      }
     }
   }
   for (int k = warp; k < kGatherTiles; k += kWarps) {
