@@ -176,6 +176,24 @@ __device__ __forceinline__ uint32_t e5m2_sm_bytes(uint32_t v12) {
   return (t * 33u) & 0x83838383u;
 }
 
+// Escape values staged per tile, compact in ordinal order (the decode warp
+// finds a value as slot_first[slot] + rank within the slot's bitmap word);
+// tiles with more escapes read the rest straight from global memory.
+constexpr int kDecValCap = 1024;
+constexpr uint32_t kNoEscape = 0xFFFFFFFFu;
+
+// Value of escape bit j of a slot: compact index = the slot's first index +
+// rank of bit j among the slot's escape bits (valid streams have ascending
+// ordinals in element order); beyond the staged capacity read global memory.
+// Corrupt streams (flagged elsewhere) only ever get a bounded read.
+__device__ __forceinline__ uint32_t escape_value(const uint8_t* vals, uint32_t first,
+                                                 uint32_t bm0, int j, uint64_t ofirst,
+                                                 uint64_t m, const uint8_t* gvals) {
+  const uint64_t c = static_cast<uint64_t>(first) + __popc(bm0 & ((1u << j) - 1u));
+  if (c < static_cast<uint64_t>(kDecValCap)) return vals[c];
+  return ofirst + c < m ? gvals[ofirst + c] : 0u;
+}
+
 // Warp-cooperative lower_bound over sorted u32 positions [0, m) (abs32 mode).
 __device__ uint64_t warp_lower_bound(const uint32_t* pos, uint64_t m, uint64_t target) {
   const int lane = threadIdx.x & 31;
@@ -475,13 +493,15 @@ constexpr int kDecOffStage = 256;                       // staged chunk offsets 
 
 template <int FMT>
 struct DecSmem {
-  static constexpr int STAGES = FMT == SZ_BF16 ? 5 : 3;
+  static constexpr int STAGES = 5;
   static constexpr int EPV = kEpv<FMT>;
   static constexpr int TILE = kDecSlots * EPV;
   alignas(128) uint8_t codes[STAGES][TILE / 2];              // <= 4-bit codes
   alignas(128) uint8_t sm[STAGES][TILE * Fmt<FMT>::kSmBits / 8];
-  alignas(16) uint8_t vals[STAGES][TILE];
   uint32_t bitmap[STAGES][TILE / 32];
+  uint32_t slot_first[STAGES][kDecSlots];  // compact index of a slot's first escape
+  uint8_t vals[STAGES][kDecValCap];        // escape values by (ordinal - ofirst)
+  uint64_t ofirst[STAGES];                 // ordinal of the tile's first escape
   uint64_t off[kDecHelpers][kDecOffStage + 1];
   uint64_t meta[STAGES];
   uint64_t full[STAGES];
@@ -597,6 +617,17 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       mbar_wait(&S.empty[s], ph ^ 1);
 #pragma unroll
       for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
+#pragma unroll
+      for (int i = lane; i < kDecSlots; i += 32) S.slot_first[s][i] = kNoEscape;
+      // Stage one in-tile escape: bitmap bit, slot's first compact index,
+      // compact value (c = ordinal - first in-tile ordinal).
+      auto stage = [&](uint64_t idx, uint64_t c, uint32_t v) {
+        const uint32_t rel = static_cast<uint32_t>(idx - s0);
+        atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
+        atomicMin(&S.slot_first[s][rel / EPV], static_cast<uint32_t>(min(c, static_cast<uint64_t>(0xFFFFFFFEu))));
+        if (c < kDecValCap) S.vals[s][c] = static_cast<uint8_t>(v);
+      };
+      uint64_t o_first = 0;
       if constexpr (ABS) {
         // abs32: per-ordinal checks spread evenly over tiles (the staging
         // below only visits ordinals whose positions land in some tile)
@@ -628,13 +659,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
         const uint64_t lo = warp_lower_bound(pos, m, s0);
         const uint64_t hi = max(lo, warp_lower_bound(pos, m, s1));
+        o_first = lo;
         for (uint64_t o = lo + lane; o < hi; o += 32) {
           const uint64_t idx = pos[o];
-          if (idx >= s0 && idx < s1) {
-            const uint32_t rel = static_cast<uint32_t>(idx - s0);
-            atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
-            S.vals[s][rel] = a.values[o];
-          }
+          if (idx >= s0 && idx < s1) stage(idx, o - lo, a.values[o]);
         }
       } else {
         const uint64_t ka = s0 / a.chunk, kb = (s1 - 1) / a.chunk;
@@ -648,6 +676,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         // 32 consecutive ordinals per round: coalesced position/value loads,
         // the predecessor's position comes from the neighbouring lane.
         uint64_t carry = 0;  // position of ordinal base-1 (previous round's lane 31)
+        bool have_first = false;
         for (uint64_t base = o_lo; base < o_hi; base += 32) {
           const uint64_t o = base + lane;
           const bool live = o < o_hi;
@@ -656,34 +685,41 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           uint64_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
           if (lane == 0) prev = carry;
           carry = __shfl_sync(0xffffffffu, pv, 31);
-          if (!live) continue;
-          // per-ordinal value checks (codec.py:451-457); complete coverage when
-          // sum(counts) != M is restored on the host (sz_check_values)
-          if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-          else if (!(p.enc_lut[v] & 0x10))
-            record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-          uint64_t lo = 0, hi = nk - 1;
-          while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (off[mid] <= o) lo = mid; else hi = mid;
+          uint64_t idx = 0;
+          bool hit = false;
+          if (live) {
+            // per-ordinal value checks (codec.py:451-457); complete coverage when
+            // sum(counts) != M is restored on the host (sz_check_values)
+            if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+            else if (!(p.enc_lut[v] & 0x10))
+              record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+            uint64_t lo = 0, hi = nk - 1;
+            while (hi - lo > 1) {
+              const uint64_t mid = (lo + hi) >> 1;
+              if (off[mid] <= o) lo = mid; else hi = mid;
+            }
+            idx = (ka + lo) * a.chunk + pv;
+            if (pv >= a.chunk) {
+              record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+            } else if (idx >= n) {
+              record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+            } else {
+              if (o > off[lo] && prev >= pv)
+                record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+              hit = idx >= s0 && idx < s1;
+            }
           }
-          if (pv >= a.chunk) {
-            record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
-            continue;
+          // the tile's escapes are a contiguous ordinal run (valid streams):
+          // its first ordinal anchors the compact value indices
+          const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+          if (!have_first && hb) {
+            o_first = base + (__ffs(hb) - 1);
+            have_first = true;
           }
-          const uint64_t idx = (ka + lo) * a.chunk + pv;
-          if (idx >= n) {
-            record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
-            continue;
-          }
-          if (o > off[lo] && prev >= pv) record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
-          if (idx >= s0 && idx < s1) {
-            const uint32_t rel = static_cast<uint32_t>(idx - s0);
-            atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
-            S.vals[s][rel] = static_cast<uint8_t>(v);
-          }
+          if (hit && o >= o_first) stage(idx, o - o_first, v);
         }
       }
+      if (lane == 0) S.ofirst[s] = o_first;
       __syncwarp();
       mbar_arrive(&S.staged[s]);
     }
@@ -702,6 +738,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
     const uint32_t sbytes = (full_slots * SBYTES) & ~15u;
     mbar_wait(&S.staged[s], ph);
+    const uint64_t ofirst = S.ofirst[s];
 #pragma unroll
     for (int i = 0; i < kDecItems; ++i) {
       const uint32_t slot = i * kThreads + tid;
@@ -764,12 +801,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
         }
         uint32_t bm = S.bitmap[s][slot];
+        const uint32_t bm0 = bm;
         while (bm) {  // rare: overwrite escaped exponent fields (bits 2-6 of the byte)
           const int j = __ffs(bm) - 1;
           bm &= bm - 1;
           const uint32_t code = (pick<CWORDS>(cw, j >> 3) >> (4 * (j & 7))) & 0xF;
           if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-          const uint32_t v = S.vals[s][slot * EPV + j];
+          const uint32_t v = escape_value(S.vals[s], S.slot_first[s][slot], bm0, j, ofirst, m,
+                                          a.values);
           const int g = j >> 2, sh = 8 * (j & 3);
 #pragma unroll
           for (int gg = 0; gg < G; ++gg)
@@ -812,6 +851,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       uint32_t bm;
       if constexpr (EPV == 32) bm = S.bitmap[s][slot];
       else bm = (S.bitmap[s][slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
+      const uint32_t bm0 = bm;
       // rare: overwrite escaped exponents (compact loop over set bits; the
       // register arrays are indexed through selects, never dynamically)
       while (bm) {
@@ -827,7 +867,8 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           code = static_cast<uint32_t>(((hi << 32) | lo) >> (bit & 31)) & 7;
         }
         if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-        const uint32_t v = S.vals[s][slot * EPV + j];
+        const uint32_t v = escape_value(S.vals[s], S.slot_first[s][slot], bm0, j, ofirst, m,
+                                        a.values);
         const int g = j >> 2, sh = 8 * (j & 3);
 #pragma unroll
         for (int gg = 0; gg < G; ++gg)
