@@ -69,6 +69,8 @@ struct EncodeArgs {
   uint64_t* base_snapshot;      // workspace copy of *escape_base for K2b
   unsigned long long* dbg;  // optional per-role cycle counters (SZ_DEBUG_TIMERS)
   uint32_t lut_stride;      // 4 (byte stride of the T4 tables; see t4_group)
+  uint32_t one;             // 1 (sum4)
+  uint32_t k_lo, k_hi;      // 1057 << 10, 1057 (e5m2_sm_hi)
 };
 
 struct EncSmem {
@@ -159,9 +161,16 @@ __device__ __forceinline__ uint32_t w_mad(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+// Sum of four lookups whose bits are disjoint (== their OR) as three IMADs
+// with the opaque kernel argument 1: the FMA pipe adds, the ALU pipe is free.
+__device__ __forceinline__ uint32_t sum4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                         uint32_t one) {
+  return w_mad(w_mad(t0, one, t1), one, w_mad(t2, one, t3));
+}
+
 template <int FMT>
 __device__ __forceinline__ uint32_t t4_group(const uint32_t (&x)[8], int g, uint32_t base,
-                                             uint32_t stride) {
+                                             uint32_t stride, uint32_t one) {
   if constexpr (FMT == SZ_E5M2 && kE5FullByte) {
     // entry address = base + 4 * byte as ONE IMAD: `stride` is the kernel
     // argument 4, opaque to ptxas, so it cannot strength-reduce the multiply
@@ -178,7 +187,7 @@ __device__ __forceinline__ uint32_t t4_group(const uint32_t (&x)[8], int g, uint
     const uint32_t t1 = lds_u32_off<128>(__byte_perm(f, base, 0x7651));
     const uint32_t t2 = lds_u32_off<256>(__byte_perm(f, base, 0x7652));
     const uint32_t t3 = lds_u32_off<384>(__byte_perm(f, base, 0x7653));
-    return t0 | t1 | t2 | t3;
+    return sum4(t0, t1, t2, t3, one);
   } else {
     const uint32_t f0 = (x[2 * g] >> 5) & 0x03FC03FCu;      // 4e of elements 4g, 4g+1
     const uint32_t f1 = (x[2 * g + 1] >> 5) & 0x03FC03FCu;  // 4e of elements 4g+2, 4g+3
@@ -186,13 +195,26 @@ __device__ __forceinline__ uint32_t t4_group(const uint32_t (&x)[8], int g, uint
     const uint32_t t1 = lds_u32_off<1024>(base + (f0 >> 16));
     const uint32_t t2 = lds_u32_off<2048>(base + (f1 & 0xFFFFu));
     const uint32_t t3 = lds_u32_off<3072>(base + (f1 >> 16));
-    return t0 | t1 | t2 | t3;
+    return sum4(t0, t1, t2, t3, one);
   }
 }
 
 // E5M2 sign|mantissa 3-bit symbols of group g as a 12-bit little-endian group
 // (formats.py:184-189 on a = sign<<2 | mantissa, formats.py:123-125): the
 // six bits of elements (0,1) gather at bits 0-5 and of (2,3) at bits 16-21.
+// The same 12-bit group at bits 20-31 of the result (bits 0-19 are junk),
+// gathered by two multiplies on the FMA pipe: after masking the sign and
+// mantissa bits of bytes 0-1 (resp. 2-3), x 1057 (= 1 + 2^5 + 2^10) moves
+// every wanted bit to its place at once — all partial products land on
+// distinct bits, so no carries — and a bit-select merges the halves.
+// k_lo = 1057 << 10 and k_hi = 1057 are kernel arguments so ptxas keeps the
+// multiplies (it would expand a literal into ALU shifts and adds).
+__device__ __forceinline__ uint32_t e5m2_sm_hi(uint32_t x, uint32_t k_lo, uint32_t k_hi) {
+  const uint32_t lo = w_mad(x & 0x00008383u, k_lo, 0u);  // symbols 0,1 -> bits 20-25
+  const uint32_t hi = w_mad(x & 0x83830000u, k_hi, 0u);  // symbols 2,3 -> bits 26-31
+  return bitselect(lo, hi, 0x03F00000u);
+}
+
 __device__ __forceinline__ uint32_t e5m2_sm12(uint32_t x) {
   const uint32_t u = (x & 0x00030003u) | ((x >> 5) & 0x001C001Cu) | ((x >> 10) & 0x00200020u);
   return (u | (u >> 10)) & 0xFFFu;
@@ -225,7 +247,7 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
     uint32_t any = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      r[g] = t4_group<FMT>(x, g, base, a.lut_stride);
+      r[g] = t4_group<FMT>(x, g, base, a.lut_stride, a.one);
       if (TAIL && nv < EPV) {  // tail slot: no codes or flags beyond N (x is 0 there)
         const int v = min(max(nv - 4 * g, 0), 4);
         r[g] &= v >= 4 ? 0xFFFFFFFFu
@@ -249,19 +271,16 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
         const uint32_t hi4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x7531);
         sw[g] = bitselect(hi4, lo4, 0x80808080u);
       }
-    } else if constexpr (kE5FullByte) {
-      // SM groups ride in bits 20-31 of each group's lookup result
-      sw[0] = (r[0] >> 20) | ((r[1] >> 8) & 0x00FFF000u) | ((r[2] << 4) & 0xFF000000u);
-      sw[1] = (r[2] >> 28) | ((r[3] >> 16) & 0x0000FFF0u) | ((r[4] >> 4) & 0x0FFF0000u) |
-              ((r[5] << 8) & 0xF0000000u);
-      sw[2] = (r[5] >> 24) | ((r[6] >> 12) & 0x000FFF00u) | (r[7] & 0xFFF00000u);
     } else {
-      uint32_t p[4];  // 24-bit SM groups of 8 elements
+      // 12-bit SM groups in bits 20-31: of each lookup result (full-byte
+      // tables) or of e5m2_sm_hi
+      uint32_t h[G];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) p[i] = e5m2_sm12(x[2 * i]) | (e5m2_sm12(x[2 * i + 1]) << 12);
-      sw[0] = p[0] | (p[1] << 24);
-      sw[1] = (p[1] >> 8) | (p[2] << 16);
-      sw[2] = (p[2] >> 16) | (p[3] << 8);
+      for (int g = 0; g < G; ++g) h[g] = kE5FullByte ? r[g] : e5m2_sm_hi(x[g], a.k_lo, a.k_hi);
+      sw[0] = (h[0] >> 20) | ((h[1] >> 8) & 0x00FFF000u) | ((h[2] << 4) & 0xFF000000u);
+      sw[1] = (h[2] >> 28) | ((h[3] >> 16) & 0x0000FFF0u) | ((h[4] >> 4) & 0x0FFF0000u) |
+              ((h[5] << 8) & 0xF0000000u);
+      sw[2] = (h[5] >> 24) | ((h[6] >> 12) & 0x000FFF00u) | (h[7] & 0xFFF00000u);
     }
     if (!TAIL || nv == EPV) {
       st_packed<CBYTES>(cdst, cw);
@@ -951,6 +970,9 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
   a.chunk_shift = (p->chunk_size & (p->chunk_size - 1)) == 0 ? __builtin_ctz(p->chunk_size) : -1;
   a.counts_mode = 0;
   a.lut_stride = 4;
+  a.one = 1;
+  a.k_lo = 1057u << 10;
+  a.k_hi = 1057u;
   a.tile_counter = w.tile_counter;
   a.tile_esc = w.tile_esc;
   a.scr_pos = w.scr_pos;

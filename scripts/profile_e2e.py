@@ -12,9 +12,12 @@ from paper_2605_01708_b200 import hostpipe  # noqa: E402
 from paper_2605_01708_b200.engine import synth_kv  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 31
-fmt = sz.ElementFormat.BF16
-bw = tuple((0x70 + i, 0.72 ** i) for i in range(16))
-words = synth_kv(n, fmt, 7, bw, tuple(range(0x10, 0x18)), 0.0016)
+fmt = sz.ElementFormat.from_name(sys.argv[2] if len(sys.argv) > 2 else "bf16")
+if fmt is sz.ElementFormat.BF16:
+    bw, esc = tuple((0x70 + i, 0.72 ** i) for i in range(16)), tuple(range(0x10, 0x18))
+else:
+    bw, esc = tuple((8 + i, 0.72 ** i) for i in range(16)), (0, 1, 2, 3, 28, 29, 30, 31)
+words = synth_kv(n, fmt, 7, bw, esc, 0.0016)
 host = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
 host.copy_(words)
 book = sz.ExponentCodebook(fmt, tuple(e for e, _ in bw), 4, sz.CodebookMode.TOPK_EXPLICIT)
@@ -30,7 +33,7 @@ def T(label, fn):
     return r
 
 
-for rep in range(2):
+for rep in range(3):
     enc = T("encode (public API)", lambda: sz.encode(sz.RawTensorStream(fmt, host), cfg))
     counts_np = T("counts to numpy", lambda: sz.codec.to_numpy(enc.chunk_counts))
     T("pinned alloc 4 GiB", lambda: torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True))
