@@ -29,6 +29,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda.h>           // CUtensorMap (types only; the encoder entry point
+#include <cudaTypedefs.h>   // comes from cudaGetDriverEntryPoint — no -lcuda)
+
 #include "sz_common.cuh"
 
 namespace sz {
@@ -70,11 +73,14 @@ struct EncodeArgs {
   unsigned long long* dbg;  // optional per-role cycle counters (SZ_DEBUG_TIMERS)
   uint32_t lut_stride;      // 4 (byte stride of the T4 tables; see t4_group)
   uint32_t one;             // 1 (sum4)
+  int32_t use_tmap;         // full tiles arrive by 2-D tensor TMA, 128B-swizzled
   uint32_t k_lo, k_hi;      // 1057 << 10, 1057 (e5m2_sm_hi)
 };
 
 struct EncSmem {
-  alignas(128) uint8_t in[kEncInStages][kEncTileBytes];
+  // 1024-aligned: the 128B-swizzle pattern of tensor TMA is a function of
+  // shared-address bits 7-9
+  alignas(1024) uint8_t in[kEncInStages][kEncTileBytes];
   uint32_t fmask[kEncScanSlots][kEncSlots];
   // escape records (tile-local element index | raw exponent << 16), in
   // arbitrary order; the writer warp derives each one's rank from fmask
@@ -364,9 +370,22 @@ __device__ __forceinline__ void put_position(uint8_t* base, uint64_t i, uint64_t
   }
 }
 
+// 2-D tensor TMA: one 128 B x 256-row box (one 32 KiB tile) into shared
+// memory with the 128B swizzle (16-byte chunk c of row r lands at chunk
+// c ^ (r & 7)), completion counted on `bar`.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x,
+                                            int32_t y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+
 template <int FMT, int CB, int POSB>
 __global__ void __launch_bounds__(kEncThreads, 1)
-    encode_tiles(const __grid_constant__ sz_params p, const EncodeArgs a) {
+    encode_tiles(const __grid_constant__ sz_params p, const EncodeArgs a,
+                 const __grid_constant__ CUtensorMap tmap) {
   constexpr int EPV = kEpv<FMT>;
   constexpr int WB = Fmt<FMT>::kWordBytes;
   constexpr uint64_t TILE = static_cast<uint64_t>(kEncSlots) * EPV;
@@ -375,7 +394,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   constexpr int SBYTES = EPV * SMB / 8;
   constexpr int PB = POSB == 0 ? 1 : POSB;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  EncSmem& S = *reinterpret_cast<EncSmem*>(smem_raw);
+  EncSmem& S = *reinterpret_cast<EncSmem*>(
+      smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
@@ -445,7 +465,11 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         const uint64_t e0 = tile * TILE;
         const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
         const uint32_t bytes = full_slots * 32;
-        if (bytes) {
+        if (a.use_tmap && e0 + TILE <= n) {
+          mbar_arrive_tx(&S.full[s], kEncTileBytes);
+          tma_load_2d(S.in[s], &tmap, 0, static_cast<int32_t>(tile * (kEncTileBytes / 128)),
+                      &S.full[s]);
+        } else if (bytes) {
           mbar_arrive_tx(&S.full[s], bytes);
           tma_load_1d(S.in[s], a.words + e0 * WB, bytes, &S.full[s]);
         } else {
@@ -486,11 +510,20 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       uint32_t x[kEncItems][8];
       int nv[kEncItems];
       if (!tail_tile) {
-        // steady state: every slot is full and in the TMA stage
+        // steady state: every slot is full and in the TMA stage.  Slot
+        // i*512 + tid is row (slot >> 2) of 128 B, 16-byte chunks 2(tid&3) and
+        // 2(tid&3)+1; with the swizzle they sit at chunk ^ (row & 7), and
+        // row & 7 = (tid >> 2) & 7 — per-thread constants.  A quarter-warp then
+        // reads 8 distinct chunks of 2 rows: no bank conflicts (the linear
+        // layout's 32-byte stride made every read 2-way conflicted).
+        const uint32_t rsw = (tid >> 2) & 7, c0 = 2 * (tid & 3);
+        const uint32_t off0 = a.use_tmap ? ((c0 ^ rsw) << 4) : (tid & 3) * 32;
+        const uint32_t off1 = a.use_tmap ? (((c0 + 1) ^ rsw) << 4) : (tid & 3) * 32 + 16;
 #pragma unroll
         for (int i = 0; i < kEncItems; ++i) {
-          const uint4* src = reinterpret_cast<const uint4*>(S.in[s] + (i * kEncDense + tid) * 32);
-          const uint4 v0 = src[0], v1 = src[1];
+          const uint8_t* row = S.in[s] + (i * kEncDense + tid) / 4 * 128;
+          const uint4 v0 = *reinterpret_cast<const uint4*>(row + off0);
+          const uint4 v1 = *reinterpret_cast<const uint4*>(row + off1);
           x[i][0] = v0.x; x[i][1] = v0.y; x[i][2] = v0.z; x[i][3] = v0.w;
           x[i][4] = v1.x; x[i][5] = v1.y; x[i][6] = v1.z; x[i][7] = v1.w;
           nv[i] = EPV;
@@ -895,14 +928,14 @@ int sm_count() {
 
 template <int FMT, int CB, int POSB>
 cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
-                          cudaStream_t s) {
+                          const CUtensorMap& tm, cudaStream_t s) {
   auto kern = encode_tiles<FMT, CB, POSB>;
-  const int smem = static_cast<int>(sizeof(EncSmem));
+  const int smem = static_cast<int>(sizeof(EncSmem)) + 1024;  // + alignment slack
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const uint64_t want = static_cast<uint64_t>(sm_count());
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
-  kern<<<grid, kEncThreads, smem, s>>>(p, a);
+  kern<<<grid, kEncThreads, smem, s>>>(p, a, tm);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups), kThreads, 0, s>>>(p, g);
@@ -911,20 +944,45 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
 
 template <int FMT, int CB>
 cudaError_t dispatch_pos(int posb, const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
-                         cudaStream_t s) {
+                         const CUtensorMap& tm, cudaStream_t s) {
   switch (posb) {
-    case 0: return launch_encode<FMT, CB, 0>(p, a, g, s);
-    case 1: return launch_encode<FMT, CB, 1>(p, a, g, s);
-    case 2: return launch_encode<FMT, CB, 2>(p, a, g, s);
-    default: return launch_encode<FMT, CB, 4>(p, a, g, s);
+    case 0: return launch_encode<FMT, CB, 0>(p, a, g, tm, s);
+    case 1: return launch_encode<FMT, CB, 1>(p, a, g, tm, s);
+    case 2: return launch_encode<FMT, CB, 2>(p, a, g, tm, s);
+    default: return launch_encode<FMT, CB, 4>(p, a, g, tm, s);
   }
 }
 
 template <int FMT>
 cudaError_t dispatch_cb(int posb, const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
+                        const CUtensorMap& tm,
                         cudaStream_t s) {
-  return p.code_bits == 4 ? dispatch_pos<FMT, 4>(posb, p, a, g, s)
-                          : dispatch_pos<FMT, 3>(posb, p, a, g, s);
+  return p.code_bits == 4 ? dispatch_pos<FMT, 4>(posb, p, a, g, tm, s)
+                          : dispatch_pos<FMT, 3>(posb, p, a, g, tm, s);
+}
+
+// Input words as a 2-D byte tensor [rows][128] (full 128-byte rows only),
+// boxes of 256 rows = one 32 KiB encoder tile, 128B swizzle.  Returns false
+// (caller falls back to 1-D bulk copies) when the driver entry point is
+// unavailable or the input has no full tile.
+bool make_input_tmap(const void* words, uint64_t n_bytes, CUtensorMap* tm) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode_fn = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode_fn || n_bytes < static_cast<uint64_t>(kEncTileBytes)) return false;
+  const cuuint64_t dims[2] = {128, n_bytes / 128};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, kEncTileBytes / 128};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode_fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(words), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -1022,11 +1080,13 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
     cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s);
     a.dbg = dbg;
   }
+  alignas(64) CUtensorMap tm{};
+  a.use_tmap = make_input_tmap(d_words, n * (p->fmt == SZ_BF16 ? 2 : 1), &tm) ? 1 : 0;
   const int posb = pos_bytes(p);
   switch (p->fmt) {
-    case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, g, s); break;
-    case SZ_E5M2: e = dispatch_cb<SZ_E5M2>(posb, *p, a, g, s); break;
-    default: e = dispatch_cb<SZ_E4M3>(posb, *p, a, g, s); break;
+    case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, g, tm, s); break;
+    case SZ_E5M2: e = dispatch_cb<SZ_E5M2>(posb, *p, a, g, tm, s); break;
+    default: e = dispatch_cb<SZ_E4M3>(posb, *p, a, g, tm, s); break;
   }
   if (e != cudaSuccess) return sz_record_cuda(e);
   if (dbg) {
