@@ -37,7 +37,8 @@ enum sz_status {
   SZ_ECONFIG = 1,   /* unsupported/inconsistent parameters (ConfigError)     */
   SZ_EWORKSPACE = 2,/* workspace too small                                   */
   SZ_EALIGN = 3,    /* a pointer is not aligned as documented                */
-  SZ_ECUDA = 4      /* a CUDA launch failed (sz_last_cuda_error() has detail) */
+  SZ_ECUDA = 4,     /* a CUDA launch failed (sz_last_cuda_error() has detail) */
+  SZ_EOUTPUT = 5    /* an output buffer is too small (sz_frame_container)     */
 };
 
 /* Codec parameters = CodecConfig (codec.py:86-135) + the codebook's LUTs
@@ -187,6 +188,22 @@ int sz_check_values(const uint8_t* d_values, uint64_t m, const sz_params* p,
 /* d_result[0] = mismatch count, d_result[1] = ~first mismatch index (0: none). */
 int sz_compare(const void* d_a, const void* d_b, uint64_t n, uint32_t word_bytes,
                uint64_t* d_result, void* stream);
+
+/* ---- SPLZ container framing (container.py:201-215, FORMATS.md:65-105) ----
+ * Byte-identical container = 28-byte header | SZCB codebook record
+ * (container.py:128-137) | counts | codes | sign-mantissa | positions |
+ * values, assembled in ONE contiguous device buffer from the sections of an
+ * encode.  M is read from enc->d_n_escapes on the device (header field,
+ * escape section lengths), so framing can be enqueued right behind sz_encode
+ * with no host round trip.  *d_nbytes (device u64) receives the container
+ * length; the caller sizes d_out with sz_container_bytes(n, capacity, p) and
+ * must have encoded with enough escape capacity (M <= enc->escape_capacity).
+ * Values come from enc->d_values (BF16) or enc->d_values_packed (FP8). */
+size_t sz_container_prefix_bytes(const sz_params* p);          /* 28 + 9 + k */
+uint64_t sz_container_bytes(uint64_t n, uint64_t m, const sz_params* p);
+int sz_frame_container(const sz_params* p, uint64_t n, const sz_encoded* enc,
+                       uint8_t* d_out, uint64_t out_capacity, uint64_t* d_nbytes,
+                       void* stream);
 
 /* ---- coverage_by_group (calibration.py:191-212): member count per group -- */
 int sz_group_members(const void* d_words, uint64_t n, const sz_params* p,

@@ -205,6 +205,23 @@ def section_bytes(sec: dict) -> list:
     ]
 
 
+def codebook_record(book, p: Params) -> bytes:
+    """SZCB record — container.py:128-137."""
+    return (b"SZCB" + bytes([1, p.fmt, p.code_bits, 1 if p.sentinel else 0, len(book)])
+            + bytes(book))
+
+
+def container_bytes(sec: dict, p: Params, book) -> bytes:
+    """SPLZ container image — container.py:201-215 (header layout
+    container.py:7-36: magic, version, format, mode, code bits, chunk u32,
+    N u64, M u64), then the codebook record and the sections."""
+    import struct
+    mode = 1 if p.sentinel else (2 if p.abs32 else 0)
+    header = b"SPLZ" + struct.pack("<BBBBIQQ", 1, p.fmt, mode, p.code_bits, p.chunk,
+                                   sec["n"], sec["m"])
+    return header + codebook_record(book, p) + b"".join(section_bytes(sec))
+
+
 def payload_bytes(n: int, m: int, p: Params) -> int:
     """codec.py:539-550."""
     wb, eb, sb = FORMATS[p.fmt]

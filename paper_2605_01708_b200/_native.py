@@ -20,7 +20,7 @@ from .errors import ConfigError, NativeError
 LIB_PATH = Path(__file__).resolve().parent / "libsz_b200.so"
 ABI_VERSION = 1
 
-SZ_OK, SZ_ECONFIG, SZ_EWORKSPACE, SZ_EALIGN, SZ_ECUDA = range(5)
+SZ_OK, SZ_ECONFIG, SZ_EWORKSPACE, SZ_EALIGN, SZ_ECUDA, SZ_EOUTPUT = range(6)
 NUM_CHECKS = 13
 (DEC_CODE_PAD, DEC_SM_PAD, DEC_VALUE_DOMAIN, DEC_VALUE_IN_BOOK, DEC_SENTINEL_COUNT,
  DEC_ABS_PAST_END, DEC_ABS_NOT_INC, DEC_COUNTS_TOTAL, DEC_POS_OVER_CHUNK,
@@ -78,6 +78,10 @@ _SIGNATURES = {
     "sz_compare": (C.c_int, [_P, _P, _U64, _U32, _P, _P]),
     "sz_group_members": (C.c_int, [_P, _U64, C.POINTER(SzParams), _U64, _P, _P]),
     "sz_synth_words": (C.c_int, [_P, _U64, _U32, _U64, _P, _P, _U32, _P]),
+    "sz_container_prefix_bytes": (C.c_size_t, [C.POINTER(SzParams)]),
+    "sz_container_bytes": (_U64, [_U64, _U64, C.POINTER(SzParams)]),
+    "sz_frame_container": (C.c_int, [C.POINTER(SzParams), _U64, C.POINTER(SzEncoded), _P, _U64,
+                                     _P, _P]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 
@@ -118,6 +122,8 @@ def check(rc: int, what: str) -> None:
         raise NativeError(f"{what}: misaligned device buffer")
     if rc == SZ_EWORKSPACE:
         raise NativeError(f"{what}: workspace too small")
+    if rc == SZ_EOUTPUT:
+        raise NativeError(f"{what}: output buffer too small")
     raise NativeError(f"{what}: CUDA error {lib.sz_last_cuda_error().decode()}")
 
 

@@ -113,6 +113,18 @@ class DeviceCodec:
         raw = self.status.cpu().numpy()
         _raise_from_status(raw, self.streams(), self.config, self.codebook, self.bufs.values)
 
+    # ------------------------------------------------------------ framing
+    def container_capacity(self) -> int:
+        """Bytes of an SPLZ container holding up to ``capacity`` escapes."""
+        return int(self.lib.sz_container_bytes(self.n, self.capacity, self.params))
+
+    def frame(self, out: torch.Tensor, nbytes_dev: torch.Tensor, stream=None) -> None:
+        """Enqueue ``sz_frame_container`` on the current sections: the SPLZ
+        file image in ``out``, its length in ``nbytes_dev`` — M is read on the
+        device, so encode -> frame -> send needs no host round trip."""
+        from .container import frame_device
+        frame_device(self.params, self.n, self.bufs.struct(), out, nbytes_dev, stream)
+
     # ------------------------------------------------------------ compare
     def compare(self, a: torch.Tensor, b: torch.Tensor, stream=None) -> torch.Tensor:
         res = torch.empty(2, dtype=torch.int64, device=self.device)

@@ -37,6 +37,7 @@ def load_reference():
 def main():
     sz = load_reference()
     from splitzip.codec import EncodedStreams
+    from splitzip import container as ref_container
 
     BF16, E5M2, E4M3 = (sz.ElementFormat.BF16, sz.ElementFormat.FP8_E5M2,
                         sz.ElementFormat.FP8_E4M3)
@@ -75,6 +76,9 @@ def main():
         for name, data in secs.items():
             arrays[p + name] = np.frombuffer(data, dtype=np.uint8)
         arrays[p + "escape_values_raw"] = np.asarray(enc.escape_values, np.uint8)
+        # the reference's SPLZ container bytes (container.py:201-215)
+        arrays[p + "container"] = np.frombuffer(
+            ref_container.container_to_bytes(enc, cfg, enc.codebook), dtype=np.uint8)
         cases.append({
             "id": cid, "tag": tag, "fmt": FMT_ID[fmt], "code_bits": code_bits,
             "sentinel": mode is SENT, "chunk": chunk, "abs32": pos == ABS,
@@ -219,10 +223,44 @@ def main():
     mutate("m_mismatch", escape_values=vals[:-1])
     mutate("clean")
 
+    # 8. Container parse verdicts (container.py:225-296) on mutated bytes of a
+    #    valid BF16 container and an E5M2 one (5-bit values section).
+    cverdicts = []
+    for base_id in ("kv_bf16_r16", "kv_e5m2_r123"):
+        good = arrays[f"{base_id}/container"].tobytes()
+        k = len(next(c for c in cases if c["id"] == base_id)["book"])
+        muts = {
+            "clean": good,
+            "bad_magic": b"SPLX" + good[4:],
+            "bad_version": good[:4] + bytes([2]) + good[5:],
+            "bad_format": good[:5] + bytes([7]) + good[6:],
+            "bad_mode": good[:6] + bytes([9]) + good[7:],
+            "bad_code_bits": good[:7] + bytes([5]) + good[8:],
+            "zero_chunk": good[:8] + bytes(4) + good[12:],
+            "zero_n": good[:12] + bytes(8) + good[20:],
+            "m_gt_n": good[:20] + (10 ** 9).to_bytes(8, "little") + good[28:],
+            "bad_cb_magic": good[:28] + b"SZCX" + good[32:],
+            "cb_mismatch_bits": good[:34] + bytes([3]) + good[35:],
+            "truncated_header": good[:20],
+            "truncated_codebook": good[:28 + 9 + k - 1],
+            "truncated_counts": good[:28 + 9 + k + 3],
+            "truncated_values": good[:-1],
+            "trailing": good + b"\x00",
+        }
+        for mid, data in muts.items():
+            try:
+                ref_container.container_from_bytes(data)
+                verdict = {"raised": None, "section": None}
+            except sz.SplitZipError as exc:
+                verdict = {"raised": type(exc).__name__,
+                           "section": getattr(exc, "section", None)}
+            arrays[f"cont_{base_id}_{mid}"] = np.frombuffer(data, dtype=np.uint8)
+            cverdicts.append({"id": f"cont_{base_id}_{mid}", "base": base_id, **verdict})
+
     np.savez_compressed(HERE / "golden.npz", **arrays)
     (HERE / "manifest.json").write_text(json.dumps(
         {"generator": "tests/golden/make_golden.py (reference splitzip 0.1.0)",
-         "cases": cases, "corruptions": corrupt}, indent=1))
+         "cases": cases, "corruptions": corrupt, "container_verdicts": cverdicts}, indent=1))
     print(f"{len(cases)} cases, {len(corrupt)} corruption verdicts, "
           f"{(HERE / 'golden.npz').stat().st_size} bytes")
 
