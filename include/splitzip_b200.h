@@ -189,6 +189,23 @@ int sz_check_values(const uint8_t* d_values, uint64_t m, const sz_params* p,
 int sz_compare(const void* d_a, const void* d_b, uint64_t n, uint32_t word_bytes,
                uint64_t* d_result, void* stream);
 
+/* ---- Paged / segmented streams (paged-KV gather) -------
+ * The logical stream is the concatenation of n_segs segments of seg_bytes
+ * each (a power of two >= 32; e.g. one vLLM KV-cache block), segment i at
+ * the 32-byte-aligned device address d_seg_addrs[i] (a device array of u64).
+ * sz_encode_segments reads the blocks in place (the producer warp's bulk
+ * copies gather them — no contiguous staging copy), N = n_segs*seg_bytes /
+ * word_bytes; its sections are byte-identical to sz_encode of the gathered
+ * words.  sz_decode_segments writes the decoded words straight into the
+ * destination blocks.  Workspaces as for sz_encode / sz_decode with that N. */
+int sz_encode_segments(const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
+                       const sz_params* p, const sz_encoded* out, void* d_ws,
+                       size_t ws_bytes, void* stream);
+int sz_decode_segments(const sz_encoded_in* in, const sz_params* p,
+                       const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
+                       sz_decode_status* d_status, void* d_ws, size_t ws_bytes,
+                       void* stream);
+
 /* ---- SPLZ container framing (container.py:201-215, FORMATS.md:65-105) ----
  * Byte-identical container = 28-byte header | SZCB codebook record
  * (container.py:128-137) | counts | codes | sign-mantissa | positions |

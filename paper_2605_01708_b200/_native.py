@@ -78,6 +78,10 @@ _SIGNATURES = {
     "sz_compare": (C.c_int, [_P, _P, _U64, _U32, _P, _P]),
     "sz_group_members": (C.c_int, [_P, _U64, C.POINTER(SzParams), _U64, _P, _P]),
     "sz_synth_words": (C.c_int, [_P, _U64, _U32, _U64, _P, _P, _U32, _P]),
+    "sz_encode_segments": (C.c_int, [_P, _U64, _U64, C.POINTER(SzParams), C.POINTER(SzEncoded),
+                                     _P, C.c_size_t, _P]),
+    "sz_decode_segments": (C.c_int, [C.POINTER(SzEncodedIn), C.POINTER(SzParams), _P, _U64, _U64,
+                                     _P, _P, C.c_size_t, _P]),
     "sz_container_prefix_bytes": (C.c_size_t, [C.POINTER(SzParams)]),
     "sz_container_bytes": (_U64, [_U64, _U64, C.POINTER(SzParams)]),
     "sz_frame_container": (C.c_int, [C.POINTER(SzParams), _U64, C.POINTER(SzEncoded), _P, _U64,

@@ -124,7 +124,22 @@ struct DecodeArgs {
   uint64_t codes_len, sm_len;
   uint32_t chunk;
   int32_t chunk_shift;
+  // Segmented (paged) output: when non-null, element
+  // byte offset o of the stream lands at seg_addrs[o >> seg_shift] + (o & mask)
+  // — decoded words go straight into the destination's KV-cache blocks.
+  const uint64_t* seg_addrs;
+  uint32_t seg_shift;
 };
+
+// Address of the 32-byte output slot starting at element e0 (slots never
+// straddle segments: segments are >= 32 bytes, powers of two).
+template <int WB>
+__device__ __forceinline__ uint8_t* out_slot(const DecodeArgs& a, uint64_t e0) {
+  if (!a.seg_addrs) return a.out + e0 * WB;
+  const uint64_t o = e0 * WB;
+  return reinterpret_cast<uint8_t*>(__ldg(a.seg_addrs + (o >> a.seg_shift))) +
+         (o & ((1ull << a.seg_shift) - 1));
+}
 
 template <int NBYTES>
 __device__ __forceinline__ void ld_packed(const uint8_t* src, uint32_t* w) {
@@ -471,7 +486,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int g = 0; g < G; ++g) rebuild_group<FMT>(eg[i][g], ag[i][g], ow, g);
     if (e0 + EPV <= n) {
-      st256(a.out + e0 * WB, ow);
+      st256(out_slot<WB>(a, e0), ow);
     } else if (e0 < n) {
       st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
     }
@@ -814,7 +829,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           for (int gg = 0; gg < G; ++gg)
             if (gg == g) ow[gg] = (ow[gg] & ~(0x7Cu << sh)) | (v << (sh + 2));
         }
-        if (nv == EPV) st256(a.out + e0 * WB, ow);
+        if (nv == EPV) st256(out_slot<WB>(a, e0), ow);
         else st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
         continue;
       }
@@ -877,7 +892,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       uint32_t ow[8];
 #pragma unroll
       for (int g = 0; g < G; ++g) rebuild_group<FMT>(eg[g], ag[g], ow, g);
-      if (nv == EPV) st256(a.out + e0 * WB, ow);
+      if (nv == EPV) st256(out_slot<WB>(a, e0), ow);
       else st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
     }
     mbar_arrive(&S.empty[s]);
@@ -995,10 +1010,17 @@ size_t sz_decode_workspace_bytes(uint64_t n, uint64_t m, const sz_params* p) {
   return carve(nullptr, n, p).total;
 }
 
-int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
-              sz_decode_status* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+// Shared body of sz_decode (contiguous output) and sz_decode_segments (paged
+// output: d_words_out null, segment table + log2 segment bytes).
+int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
+                const uint64_t* seg_addrs, uint32_t seg_shift, sz_decode_status* d_status,
+                void* d_ws, size_t ws_bytes, void* stream) {
   if (int rc = sz_check_params(p, 1)) return rc;
-  if (!in || !d_words_out || !d_status || in->n_elements == 0) return SZ_ECONFIG;
+  if (!in || (!d_words_out && !seg_addrs) || !d_status || in->n_elements == 0)
+    return SZ_ECONFIG;
   if (!in->d_n_escapes && in->n_escapes > in->n_elements) return SZ_ECONFIG;
   const uint64_t n = in->n_elements, m = in->d_n_escapes ? n : in->n_escapes;
   if ((reinterpret_cast<uintptr_t>(d_words_out) & 31) ||
@@ -1044,6 +1066,8 @@ int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   a.n = n;
   a.m = m;
   a.out = static_cast<uint8_t*>(d_words_out);
+  a.seg_addrs = seg_addrs;
+  a.seg_shift = seg_shift;
   a.status = d_status;
   a.states = w.dec_states;
   a.tile_counter = w.dec_counter;
@@ -1060,6 +1084,27 @@ int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
     default: e = dec_cb<SZ_E4M3>(posb, *p, a, s); break;
   }
   return e == cudaSuccess ? SZ_OK : sz_record_cuda(e);
+}
+}  // namespace
+
+extern "C" {
+
+int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
+              sz_decode_status* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_words_out) return SZ_ECONFIG;
+  return decode_impl(in, p, d_words_out, nullptr, 0, d_status, d_ws, ws_bytes, stream);
+}
+
+int sz_decode_segments(const sz_encoded_in* in, const sz_params* p, const uint64_t* d_seg_addrs,
+                       uint64_t n_segs, uint64_t seg_bytes, sz_decode_status* d_status,
+                       void* d_ws, size_t ws_bytes, void* stream) {
+  if (!p || !in || !d_seg_addrs || n_segs == 0 || seg_bytes < 32 ||
+      (seg_bytes & (seg_bytes - 1)))
+    return SZ_ECONFIG;
+  const uint64_t wb = p->fmt == SZ_BF16 ? 2 : 1;
+  if (in->n_elements != n_segs * seg_bytes / wb) return SZ_ECONFIG;
+  return decode_impl(in, p, nullptr, d_seg_addrs, static_cast<uint32_t>(__builtin_ctzll(seg_bytes)),
+                     d_status, d_ws, ws_bytes, stream);
 }
 
 int sz_check_values(const uint8_t* d_values, uint64_t m, const sz_params* p,

@@ -74,6 +74,10 @@ struct EncodeArgs {
   uint32_t lut_stride;      // 4 (byte stride of the T4 tables; see t4_group)
   uint32_t one;             // 1 (sum4)
   int32_t use_tmap;         // full tiles arrive by 2-D tensor TMA, 128B-swizzled
+  // Segmented (paged) input: when non-null the logical
+  // stream is segment i (2^seg_shift bytes) at seg_addrs[i], i = 0, 1, ...
+  const uint64_t* seg_addrs;
+  uint32_t seg_shift;
   uint32_t k_lo, k_hi;      // 1057 << 10, 1057 (e5m2_sm_hi)
 };
 
@@ -465,7 +469,22 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         const uint64_t e0 = tile * TILE;
         const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
         const uint32_t bytes = full_slots * 32;
-        if (a.use_tmap && e0 + TILE <= n) {
+        if (a.seg_addrs) {
+          // paged KV: one bulk copy per (tile ∩ segment) piece, straight from
+          // the cache blocks — no gather pass through HBM
+          if (bytes) mbar_arrive_tx(&S.full[s], bytes);
+          else mbar_arrive(&S.full[s]);
+          const uint64_t b0 = e0 * WB, seg_mask = (1ull << a.seg_shift) - 1;
+          for (uint32_t o = 0; o < bytes;) {
+            const uint64_t g = b0 + o;
+            const uint32_t len = static_cast<uint32_t>(
+                min(static_cast<uint64_t>(bytes - o), (seg_mask + 1) - (g & seg_mask)));
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(
+                                     __ldg(a.seg_addrs + (g >> a.seg_shift))) + (g & seg_mask);
+            tma_load_1d(S.in[s] + o, src, len, &S.full[s]);
+            o += len;
+          }
+        } else if (a.use_tmap && e0 + TILE <= n) {
           mbar_arrive_tx(&S.full[s], kEncTileBytes);
           tma_load_2d(S.in[s], &tmap, 0, static_cast<int32_t>(tile * (kEncTileBytes / 128)),
                       &S.full[s]);
@@ -690,6 +709,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
 // ------------------------------------------------------------------ K2b
 struct GatherArgs {
   const uint8_t* words;
+  const uint64_t* seg_addrs;  // segmented input (or null)
+  uint32_t seg_shift;
   uint64_t n;
   const uint32_t* tile_esc;
   const uint8_t* scr_pos;
@@ -824,7 +845,13 @@ __global__ void __launch_bounds__(kThreads)
         uint32_t ev = 0;
         bool esc = false;
         if (idx < e_end) {
-          const uint32_t w = WB == 2 ? reinterpret_cast<const uint16_t*>(a.words)[idx] : a.words[idx];
+          const uint8_t* wp = a.words + idx * WB;
+          if (a.seg_addrs) {
+            const uint64_t off = idx * WB;
+            wp = reinterpret_cast<const uint8_t*>(a.seg_addrs[off >> a.seg_shift]) +
+                 (off & ((1ull << a.seg_shift) - 1));
+          }
+          const uint32_t w = WB == 2 ? *reinterpret_cast<const uint16_t*>(wp) : *wp;
           ev = raw_exponent<FMT>(w);
           esc = (lut[ev] & 0x10) != 0;
         }
@@ -997,10 +1024,16 @@ size_t sz_encode_workspace_bytes(uint64_t n, const sz_params* p) {
   return carve(nullptr, n, p).total + 256;
 }
 
-int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_encoded* out,
-              void* d_ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+// Shared body of sz_encode (contiguous words) and sz_encode_segments (paged:
+// d_words null, segment table + log2 segment bytes).
+int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shift, uint64_t n,
+                const sz_params* p, const sz_encoded* out, void* d_ws, size_t ws_bytes,
+                void* stream) {
   if (int rc = sz_check_params(p, 0)) return rc;
-  if (n == 0 || !out || !d_words) return SZ_ECONFIG;
+  if (n == 0 || !out || (!d_words && !seg_addrs)) return SZ_ECONFIG;
   if ((reinterpret_cast<uintptr_t>(d_words) & 31) ||
       (reinterpret_cast<uintptr_t>(out->d_codes) & 15) ||
       (reinterpret_cast<uintptr_t>(out->d_sm) & 15) || (reinterpret_cast<uintptr_t>(d_ws) & 255))
@@ -1016,6 +1049,8 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
 
   EncodeArgs a{};
   a.words = static_cast<const uint8_t*>(d_words);
+  a.seg_addrs = seg_addrs;
+  a.seg_shift = seg_shift;
   a.n = n;
   a.codes = static_cast<uint8_t*>(out->d_codes);
   a.sm = static_cast<uint8_t*>(out->d_sm);
@@ -1046,6 +1081,8 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
 
   GatherArgs g{};
   g.words = a.words;
+  g.seg_addrs = seg_addrs;
+  g.seg_shift = seg_shift;
   g.n = n;
   g.tile_esc = w.tile_esc;
   g.scr_pos = w.scr_pos;
@@ -1081,7 +1118,7 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
     a.dbg = dbg;
   }
   alignas(64) CUtensorMap tm{};
-  a.use_tmap = make_input_tmap(d_words, n * (p->fmt == SZ_BF16 ? 2 : 1), &tm) ? 1 : 0;
+  a.use_tmap = !seg_addrs && make_input_tmap(d_words, n * (p->fmt == SZ_BF16 ? 2 : 1), &tm);
   const int posb = pos_bytes(p);
   switch (p->fmt) {
     case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, g, tm, s); break;
@@ -1109,6 +1146,25 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
   return SZ_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_encoded* out,
+              void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_words) return SZ_ECONFIG;
+  return encode_impl(d_words, nullptr, 0, n, p, out, d_ws, ws_bytes, stream);
+}
+
+int sz_encode_segments(const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
+                       const sz_params* p, const sz_encoded* out, void* d_ws, size_t ws_bytes,
+                       void* stream) {
+  if (!p || !d_seg_addrs || n_segs == 0 || seg_bytes < 32 || (seg_bytes & (seg_bytes - 1)))
+    return SZ_ECONFIG;
+  const uint64_t wb = p->fmt == SZ_BF16 ? 2 : 1;
+  return encode_impl(nullptr, d_seg_addrs, static_cast<uint32_t>(__builtin_ctzll(seg_bytes)),
+                     n_segs * seg_bytes / wb, p, out, d_ws, ws_bytes, stream);
 }
 
 }  // extern "C"

@@ -1,0 +1,86 @@
+"""Paged-KV encode/decode (sz_encode_segments / sz_decode_segments): sections
+byte-identical to ``encode`` of the gathered words, and a bit-exact decode
+straight into a receiver's own blocks."""
+
+from __future__ import annotations
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+BF16_BOOK = tuple((0x70 + i, 0.72 ** i) for i in range(16))
+BF16_ESC = tuple(range(0x10, 0x18))
+E5_BOOK = tuple((8 + i, 0.72 ** i) for i in range(16))
+E5_ESC = (0, 1, 2, 3, 28, 29, 30, 31)
+
+
+def sz():
+    import paper_2605_01708_b200 as m
+    return m
+
+
+def _sel(c, ids):
+    """c[ids] for uint16/uint8 caches (index kernels lack UInt16)."""
+    v = c.view(torch.int16) if c.dtype == torch.uint16 else c.view(torch.int8)
+    return v[ids].view(c.dtype)
+
+
+def make(fmt_name, block_shape, layers, num_blocks, rate, mode="explicit", chunk=1024,
+         seed=3):
+    m = sz()
+    from paper_2605_01708_b200.engine import synth_kv
+    fmt = m.ElementFormat.from_name(fmt_name)
+    bw, esc = (BF16_BOOK, BF16_ESC) if fmt is m.ElementFormat.BF16 else (E5_BOOK, E5_ESC)
+    per_block = 1
+    for d in block_shape:
+        per_block *= d
+    caches = [synth_kv(num_blocks * per_block, fmt, seed + l, bw, esc, rate)
+              .view(num_blocks, *block_shape) for l in range(layers)]
+    cmode = m.CodebookMode.from_name(mode)
+    entries = tuple(e for e, _ in bw)[: 15 if mode == "sentinel" else 16]
+    book = m.ExponentCodebook(fmt, entries, 4, cmode)
+    cfg = m.CodecConfig(fmt, 4, cmode, chunk, codebook=book)
+    return m, fmt, caches, cfg
+
+
+@pytest.mark.parametrize("fmt_name,block_shape,rate,mode,chunk", [
+    ("bf16", (2, 16, 8, 128), 0.0016, "explicit", 1024),    # vLLM block, 64 KiB (> tile)
+    ("bf16", (2, 16, 1, 64), 0.0123, "explicit", 256),      # 4 KiB blocks (< tile)
+    ("e5m2", (2, 16, 8, 128), 0.0016, "explicit", 1024),    # 32 KiB = one FP8 tile
+    ("e5m2", (2, 4, 2, 32), 0.05, "explicit", 3000),        # 1 KiB blocks, odd chunk
+    ("bf16", (2, 16, 4, 64), 0.5, "explicit", 1024),        # escape-heavy: K2b re-derives
+    ("bf16", (2, 16, 8, 128), 0.0027, "sentinel", 1024),    # sentinel decode kernel
+])
+def test_paged_sections_and_roundtrip(fmt_name, block_shape, rate, mode, chunk):
+    from paper_2605_01708_b200 import paged
+    m, fmt, caches, cfg = make(fmt_name, block_shape, 3, 40, rate, mode, chunk)
+    g = torch.Generator().manual_seed(7)
+    ids = torch.randperm(40, generator=g)[:23].cuda()
+    gathered = torch.cat([_sel(c, ids).reshape(-1) for c in caches])
+    ref = m.encode(m.RawTensorStream(fmt, gathered), cfg)
+    enc = paged.encode_kv_blocks(caches, ids, cfg)
+    assert enc.n_escapes == ref.n_escapes
+    assert dict(enc.section_bytes()) == dict(ref.section_bytes())
+    # decode into a different pool with a different block table
+    dst = [torch.zeros_like(c) for c in caches]
+    ids2 = torch.randperm(40, generator=g)[:23].cuda()
+    paged.decode_kv_blocks(enc, cfg, enc.codebook, dst, ids2)
+    back = torch.cat([_sel(c, ids2).reshape(-1) for c in dst])
+    assert torch.equal(back, gathered)
+    # untouched blocks stay untouched
+    mask = torch.ones(40, dtype=torch.bool)
+    mask[ids2.cpu()] = False
+    for c in dst:
+        assert not bool(_sel(c, mask.nonzero().reshape(-1).cuda()).view(torch.uint8).any())
+
+
+def test_paged_rejects_bad_blocks():
+    from paper_2605_01708_b200 import paged
+    m, fmt, caches, cfg = make("bf16", (3, 16, 8, 128), 1, 8, 0.0016)   # 96 KiB: not 2^k
+    with pytest.raises(m.ConfigError):
+        paged.encode_kv_blocks(caches, torch.arange(4, device="cuda"), cfg)
+    m, fmt, caches, cfg = make("bf16", (2, 16, 8, 128), 1, 8, 0.0016)
+    nobook = m.CodecConfig(fmt)
+    with pytest.raises(m.ConfigError):
+        paged.encode_kv_blocks(caches, torch.arange(4, device="cuda"), nobook)
