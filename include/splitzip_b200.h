@@ -206,6 +206,27 @@ int sz_decode_segments(const sz_encoded_in* in, const sz_params* p,
                        sz_decode_status* d_status, void* d_ws, size_t ws_bytes,
                        void* stream);
 
+/* ---- Fused encode -> NVLink handoff flags -------------
+ * The sender encodes with its sz_encoded outputs pointing INTO the receiver's
+ * memory (peer-access / IPC-mapped pointers), so the encoder's own stores
+ * carry the compressed sections over NVLink, then sz_peer_signal raises a
+ * flag in the receiver's memory (system-scope fence + release store, after
+ * every prior kernel on `stream`).  The receiver enqueues sz_peer_wait
+ * (system-scope acquire polling until *d_flag >= value) before its decode.
+ * A wait gives up after timeout_ns (0 = 30 s) and sets *d_timed_out. */
+int sz_peer_signal(uint64_t* d_flag, uint64_t value, void* stream);
+int sz_peer_wait(const uint64_t* d_flag, uint64_t value, uint64_t timeout_ns,
+                 uint32_t* d_timed_out, void* stream);
+/* A dedicated zero-filled device region (cudaMalloc) and its CUDA IPC
+ * handle (64 bytes) so another process can map it (sz_ipc_import opens it
+ * with lazy peer access: NVLink/NVSwitch between GPUs, plain device memory on
+ * the same GPU). */
+int sz_device_alloc(uint64_t bytes, void** d_out);
+int sz_device_free(void* d);
+int sz_ipc_export(const void* d_base, uint8_t* handle_out);
+int sz_ipc_import(const uint8_t* handle, void** d_base_out);
+int sz_ipc_close(void* d_base);
+
 /* ---- SPLZ container framing (container.py:201-215, FORMATS.md:65-105) ----
  * Byte-identical container = 28-byte header | SZCB codebook record
  * (container.py:128-137) | counts | codes | sign-mantissa | positions |

@@ -82,6 +82,13 @@ _SIGNATURES = {
                                      _P, C.c_size_t, _P]),
     "sz_decode_segments": (C.c_int, [C.POINTER(SzEncodedIn), C.POINTER(SzParams), _P, _U64, _U64,
                                      _P, _P, C.c_size_t, _P]),
+    "sz_peer_signal": (C.c_int, [_P, _U64, _P]),
+    "sz_peer_wait": (C.c_int, [_P, _U64, _U64, _P, _P]),
+    "sz_device_alloc": (C.c_int, [_U64, C.POINTER(C.c_void_p)]),
+    "sz_device_free": (C.c_int, [_P]),
+    "sz_ipc_export": (C.c_int, [_P, _P]),
+    "sz_ipc_import": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
+    "sz_ipc_close": (C.c_int, [_P]),
     "sz_container_prefix_bytes": (C.c_size_t, [C.POINTER(SzParams)]),
     "sz_container_bytes": (_U64, [_U64, _U64, C.POINTER(SzParams)]),
     "sz_frame_container": (C.c_int, [C.POINTER(SzParams), _U64, C.POINTER(SzEncoded), _P, _U64,
