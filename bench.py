@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=20260517)
+    ap.add_argument("--no-handoff", action="store_true",
+                    help="skip the N>=2 prefill->decode handoff leg (config 5)")
     return ap.parse_args()
 
 
@@ -355,6 +357,9 @@ def run_ours(args) -> None:
         "clocks": clocks,
     }
 
+    if world >= 2 and world % 2 == 0 and not args.no_handoff and wl["fmt_id"] == 0:
+        line["handoff"] = handoff_leg(rank, world)
+
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m)
     if rank == 0:
@@ -362,6 +367,27 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def handoff_leg(rank: int, world: int) -> dict:
+    """Config 5 at N >= 2: pairs (2i -> 2i+1) hand 2 GiB of BF16 KV over in
+    64 MiB pieces — raw NCCL P2P vs the fused encode -> peer-store -> decode
+    link (peer.py) — for realistic and escape-heavy exponent statistics.
+    Reported beside the headline; never allowed to take the run down."""
+    import datetime
+
+    import torch.distributed as dist
+    sys.path.insert(0, str(ROOT / "scripts"))
+    try:
+        from bench_handoff import handoff_bench
+        gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=120))
+        res = handoff_bench(1 << 30, 1 << 25, 3, False, rank, world, obj_group=gloo,
+                            timeout_s=20.0)
+        res["pairs"] = world // 2
+        res["unit"] = "GB/s of BF16 KV per pair (raw bytes / max device time over ranks)"
+        return res
+    except Exception as exc:  # noqa: BLE001
+        return {"error": repr(exc)[:300]}
 
 
 def cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m) -> dict:

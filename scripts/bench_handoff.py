@@ -30,7 +30,8 @@ ESC = tuple(range(0x10, 0x18))
 
 
 def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, world: int = 1,
-                  group=None) -> dict:
+                  group=None, obj_group=None, timeout_s: float = 30.0,
+                  raw_baseline: bool = True) -> dict:
     fmt = sz.ElementFormat.BF16
     book = sz.ExponentCodebook(fmt, tuple(e for e, _ in BOOK), 4, sz.CodebookMode.TOPK_EXPLICIT)
     cfg = sz.CodecConfig(fmt, codebook=book)
@@ -38,6 +39,14 @@ def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, 
     res = {"bytes": raw, "piece_elems": piece, "reps": reps}
     sender = (rank % 2 == 0)
     partner = rank + 1 if sender else rank - 1
+
+    def agree(ok: bool) -> bool:
+        """All ranks vote (CPU group, bounded by its timeout)."""
+        if loopback or world == 1:
+            return ok
+        t = torch.tensor([int(ok)])
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=obj_group)
+        return bool(t.item())
 
     def max_ms(ms):
         if loopback or world == 1:
@@ -62,7 +71,7 @@ def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, 
         words = synth_kv(n, fmt, 11 + rank // 2, BOOK, ESC, rate)
         out = torch.empty_like(words)
         entry = {}
-        if not loopback:
+        if not loopback and raw_baseline:
             # raw baseline: NCCL P2P of the BF16 words in the same pieces
             def raw_send():
                 ops = []
@@ -75,7 +84,8 @@ def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, 
             raw_send()
             entry["raw_nccl_gbs"] = round(raw / (timed(raw_send) / 1e3) / 1e9, 1)
         if loopback:
-            snd, rcv = peer.connect_pair("send", 0, piece, cfg, book, slots=2, loopback=True)
+            snd, rcv = peer.connect_pair("send", 0, piece, cfg, book, slots=2, loopback=True,
+                                         timeout_s=timeout_s)
             s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
             def codec():
@@ -84,8 +94,14 @@ def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, 
                 torch.cuda.current_stream().wait_stream(s1)
                 torch.cuda.current_stream().wait_stream(s2)
         else:
-            link = peer.connect_pair("send" if sender else "recv", partner, piece, cfg, book,
-                                     slots=2, group=group)
+            link, err = None, None
+            try:
+                link = peer.connect_pair("send" if sender else "recv", partner, piece, cfg,
+                                         book, slots=2, group=obj_group, timeout_s=timeout_s)
+            except Exception as exc:  # noqa: BLE001 — every rank must reach the vote
+                err = exc
+            if not agree(err is None):
+                raise RuntimeError(f"peer link setup failed on some rank: {err!r}")
 
             def codec():
                 if sender:
@@ -107,6 +123,9 @@ def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, 
             link.close()
             dist.barrier(group=group)
             link.release()
+            ok = torch.tensor([int(entry.get("bitexact", True))], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            entry["bitexact"] = bool(ok.item())
         m = int(sz.encode(sz.RawTensorStream(fmt, words[:1 << 24]), cfg).n_escapes)
         entry["escape_rate"] = round(m / (1 << 24), 5)
         res[tag] = entry
@@ -119,20 +138,32 @@ def main():
     ap.add_argument("--elems", type=int, default=1 << 30)       # 2 GiB of BF16 per pair
     ap.add_argument("--piece", type=int, default=1 << 25)       # 64 MiB pieces
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the multi-process path with every rank on one GPU "
+                         "(no raw NCCL baseline)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
     if args.loopback:
         res = handoff_bench(args.elems, args.piece, args.reps, True)
         res["mode"] = "loopback: sender and receiver on one GPU (no NVLink)"
     else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         if world % 2:
             raise SystemExit("needs an even number of ranks (pairs 2i -> 2i+1)")
-        res = handoff_bench(args.elems, args.piece, args.reps, False, rank, world)
-        res["mode"] = f"{world // 2} concurrent pair(s) 2i -> 2i+1 over NVLink"
+        import datetime
+        gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=120))
+        res = handoff_bench(args.elems, args.piece, args.reps, False, rank, world,
+                            obj_group=gloo, raw_baseline=args.backend == "nccl")
+        res["mode"] = (f"{world // 2} concurrent pair(s) 2i -> 2i+1 over NVLink"
+                       if args.backend == "nccl" else
+                       "gloo test mode: every rank on one GPU (time-sliced; not a measurement)")
+        res["pairs"] = world // 2
     if rank == 0:
         print(json.dumps(res), flush=True)
     if not args.loopback:
