@@ -692,25 +692,12 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         // the predecessor's position comes from the neighbouring lane.
         uint64_t carry = 0;  // position of ordinal base-1 (previous round's lane 31)
         bool have_first = false;
-        // 4 x 32 consecutive ordinals per round: every position/value load of
-        // the round is in flight before the first is used (escape-heavy tiles
-        // are latency-bound here); predecessors come from the neighbouring lane.
-        constexpr int U = 4;
-        for (uint64_t base = o_lo; base < o_hi; base += 32 * U) {
-          uint64_t pvs[U];
-          uint32_t vs[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint64_t o = base + 32 * u + lane;
-            pvs[u] = o < o_hi ? load_pos<POSB>(a.positions, o) : 0;
-            vs[u] = o < o_hi ? a.values[o] : 0;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-          const uint64_t o = base + 32 * u + lane;
+        // One ordinal per lane per round; escape-heavy ranges keep 4 x 32
+        // ordinals per round in flight (all loads before the first use), the
+        // common sparse case stays at one short round.
+        auto one = [&](uint64_t rbase, uint64_t pv, uint32_t v) {
+          const uint64_t o = rbase + lane;
           const bool live = o < o_hi;
-          const uint64_t pv = pvs[u];
-          const uint32_t v = vs[u];
           uint64_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
           if (lane == 0) prev = carry;
           carry = __shfl_sync(0xffffffffu, pv, 31);
@@ -742,11 +729,28 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           // its first ordinal anchors the compact value indices
           const uint32_t hb = __ballot_sync(0xffffffffu, hit);
           if (!have_first && hb) {
-            o_first = base + 32 * u + (__ffs(hb) - 1);
+            o_first = rbase + (__ffs(hb) - 1);
             have_first = true;
           }
           if (hit && o >= o_first) stage(idx, o - o_first, v);
+        };
+        constexpr int U = 4;
+        uint64_t base = o_lo;
+        for (; base + 32 * U <= o_hi; base += 32 * U) {
+          uint64_t pvs[U];
+          uint32_t vs[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            pvs[u] = load_pos<POSB>(a.positions, base + 32 * u + lane);
+            vs[u] = a.values[base + 32 * u + lane];
           }
+#pragma unroll
+          for (int u = 0; u < U; ++u) one(base + 32 * u, pvs[u], vs[u]);
+        }
+        for (; base < o_hi; base += 32) {
+          const uint64_t o = base + lane;
+          one(base, o < o_hi ? load_pos<POSB>(a.positions, o) : 0,
+              o < o_hi ? a.values[o] : 0u);
         }
       }
       if (lane == 0) S.ofirst[s] = o_first;
