@@ -352,7 +352,9 @@ def run_ours(args) -> None:
         "e2e": {"value": round(world * raw * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                 "api": "paper_2605_01708_b200.encode/decode on pinned host words"},
-        "gpu_launches": K * (4 + (1 if fmt.exp_bits != 8 else 0)),
+        # per step: K2a encode_tiles, K2b escape_gather, K2c escape_heavy
+        # (+ K6 pack_values for FP8), K3 offsets_kernel, K4 decode_persistent
+        "gpu_launches": K * (5 + (1 if fmt.exp_bits != 8 else 0)),
         "calibration_histogram_gbs": round(hist_gbs, 1),
         "clocks": clocks,
     }
