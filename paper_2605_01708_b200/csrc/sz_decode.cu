@@ -556,19 +556,16 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     s_lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
   const uint32_t lut2_base = smem_addr(s_lut2);
-  // E5M2 with 4-bit codes: two pair tables indexed by a code byte (elements
-  // 2i, 2i+1) whose entries hold both exponents already at their E5M2 bit
-  // positions (bits 2-6 of bytes 0/1, resp. 2/3) — reconstruct
-  // (formats.py:136-155) becomes lookup | lookup | sign-mantissa bits.
+  // E5M2 with 4-bit codes: a pair table indexed by a code byte (elements
+  // 2i, 2i+1) whose u16 entries hold both exponents already at their E5M2
+  // bit positions (bits 2-6 of each byte) — reconstruct (formats.py:136-155)
+  // becomes two lookups, one byte permute and the sign-mantissa bits.
   constexpr bool kE5Fast = FMT == SZ_E5M2 && CB == 4;
-  __shared__ __align__(1024) uint32_t s_e5[kE5Fast ? 512 : 1];
+  __shared__ __align__(1024) uint16_t s_e5[kE5Fast ? 256 : 2];
   const uint8_t* e5tab = reinterpret_cast<const uint8_t*>(s_e5);
   if constexpr (kE5Fast) {
-    for (int i = tid; i < 512; i += kDecThreads) {
-      const uint32_t b = i & 255, sh = i >= 256 ? 16 : 0;
-      s_e5[i] = ((static_cast<uint32_t>(p.dec_lut[b & 15]) << 2) |
-                 (static_cast<uint32_t>(p.dec_lut[b >> 4]) << 10)) << sh;
-    }
+    for (int b = tid; b < 256; b += kDecThreads)
+      s_e5[b] = static_cast<uint16_t>((p.dec_lut[b & 15] << 2) | (p.dec_lut[b >> 4] << 10));
   }
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -815,10 +812,13 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint32_t w = cw[g >> 1];
-          const uint32_t blo = (g & 1) ? ((w >> 14) & 0x3FCu) : ((w << 2) & 0x3FCu);
-          const uint32_t bhi = (g & 1) ? ((w >> 22) & 0x3FCu) : ((w >> 6) & 0x3FCu);
-          const uint32_t ex = *reinterpret_cast<const uint32_t*>(e5tab + blo) |
-                              *reinterpret_cast<const uint32_t*>(e5tab + 1024 + bhi);
+          // u16 entries: the 64 commonest code pairs (both codes < 16, the
+          // second < 4 — codes are frequency-ranked) sit in 32 distinct banks
+          const uint32_t blo = (g & 1) ? ((w >> 15) & 0x1FEu) : ((w << 1) & 0x1FEu);
+          const uint32_t bhi = (g & 1) ? ((w >> 23) & 0x1FEu) : ((w >> 7) & 0x1FEu);
+          const uint32_t ex = __byte_perm(*reinterpret_cast<const uint16_t*>(e5tab + blo),
+                                          *reinterpret_cast<const uint16_t*>(e5tab + bhi),
+                                          0x5410);
           ow[g] = ex | e5m2_sm_bytes(group_bits<12>(sw, g));
         }
         if (check_range) {  // codebook < 16 entries: flag codes past its end
