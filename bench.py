@@ -287,8 +287,10 @@ def run_ours(args) -> None:
     t_enc = t_dec = 0.0
     barrier()
     t0 = time.perf_counter()
+    per_step = []
     for _ in range(e2e_steps):
         pay, dec, te, td = e2e_step()
+        per_step.append((round(te * 1e3, 1), round(td * 1e3, 1)))
         h2d += raw + pay
         d2h += pay + raw
         t_enc += te
@@ -298,7 +300,8 @@ def run_ours(args) -> None:
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     assert ok
     print(f"[bench] e2e per step: encode {t_enc / e2e_steps * 1e3:.1f} ms, "
-          f"decode {t_dec / e2e_steps * 1e3:.1f} ms", file=sys.stderr)
+          f"decode {t_dec / e2e_steps * 1e3:.1f} ms; steps (enc, dec) ms: {per_step}",
+          file=sys.stderr)
     clocks = sampler.stop()
 
     # ---- roofline of the dominant kernel

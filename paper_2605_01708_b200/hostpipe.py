@@ -6,7 +6,7 @@ idles during both copies.  This module cuts the stream into chunk-aligned
 pieces (chunk-relative sections of chunk-aligned pieces concatenate exactly:
 counts, code and sign|mantissa planes, positions; the escape ordinals are
 made global on the device by the encoder's append mode, ``d_escape_base``)
-and runs three CUDA streams — H2D copy, codec kernels, D2H copy — over two
+and runs three CUDA streams — H2D copy, codec kernels, D2H copy — over three
 device buffers per plane, so PCIe in, the kernels and PCIe out overlap.
 Host outputs land directly in pinned buffers.
 """
@@ -26,6 +26,7 @@ from .codec import (CodecConfig, EncodedStreams, _config_params, _nbytes, defaul
 from .formats import pack_bits_device
 
 PIECE_ELEMS = 1 << 26   # 128 MiB of BF16 per piece
+NBUF = 3                # device buffer sets in flight (H2D | kernel | D2H)
 
 
 def piece_size(config: CodecConfig, n: int) -> int:
@@ -81,10 +82,10 @@ def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCo
     codes_h = torch.empty(packed_nbytes(n, cb), dtype=torch.uint8, pin_memory=True)
     sm_h = torch.empty(config.sm_nbytes(n), dtype=torch.uint8, pin_memory=True)
     counts_h = torch.empty(config.n_chunks(n), dtype=torch.uint32, pin_memory=True)
-    words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(2)]
-    codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(2)]
-    sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(2)]
-    cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(2)]
+    words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(NBUF)]
+    codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
+    sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
+    cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(NBUF)]
     pos_d = torch.empty(cap, dtype=config.position_torch_dtype, device=dev)
     val_d = torch.empty(cap, dtype=torch.uint8, device=dev)
     base_d = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -95,20 +96,20 @@ def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCo
     cur = torch.cuda.current_stream()
     for s in (st.h2d, st.comp, st.d2h):
         s.wait_stream(cur)
-    ev_h2d = [torch.cuda.Event() for _ in range(2)]
-    ev_enc = [torch.cuda.Event() for _ in range(2)]
-    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    ev_h2d = [torch.cuda.Event() for _ in range(NBUF)]
+    ev_enc = [torch.cuda.Event() for _ in range(NBUF)]
+    ev_d2h = [torch.cuda.Event() for _ in range(NBUF)]
     for i in range(npieces):
-        b = i % 2
+        b = i % NBUF
         lo, hi = i * P, min(n, (i + 1) * P)
         k = hi - lo
         with torch.cuda.stream(st.h2d):
-            if i >= 2:
+            if i >= NBUF:
                 st.h2d.wait_event(ev_enc[b])
             words_d[b][:k].copy_(words_h[lo:hi], non_blocking=True)
             ev_h2d[b].record(st.h2d)
         st.comp.wait_event(ev_h2d[b])
-        if i >= 2:
+        if i >= NBUF:
             st.comp.wait_event(ev_d2h[b])
         out = N.SzEncoded()
         out.d_codes, out.d_sm = N.ptr(codes_d[b]), N.ptr(sm_d[b])
@@ -165,13 +166,13 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     # ordinal offset of every piece = escapes in the chunks before it
     prefix = np.concatenate([[0], np.cumsum(counts_np.astype(np.int64))])
     out_h = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
-    codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(2)]
-    sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(2)]
-    cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(2)]
-    words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(2)]
+    codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
+    sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
+    cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(NBUF)]
+    words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(NBUF)]
     status = torch.empty((npieces, N.STATUS_BYTES), dtype=torch.uint8, device=dev)
     ws = [torch.empty(lib.sz_decode_workspace_bytes(P, 0, params), dtype=torch.uint8, device=dev)
-          for _ in range(2)]
+          for _ in range(NBUF)]
 
     st = _Streams()
     cur = torch.cuda.current_stream()
@@ -182,18 +183,18 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
                  .to(dev, non_blocking=True) if m else None)
         val_d = host_tensor(streams.escape_values, torch.uint8).to(dev, non_blocking=True) \
             if m else None
-    ev_h2d = [torch.cuda.Event() for _ in range(2)]
-    ev_dec = [torch.cuda.Event() for _ in range(2)]
-    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    ev_h2d = [torch.cuda.Event() for _ in range(NBUF)]
+    ev_dec = [torch.cuda.Event() for _ in range(NBUF)]
+    ev_d2h = [torch.cuda.Event() for _ in range(NBUF)]
     pbytes = config.position_nbytes
     for i in range(npieces):
-        b = i % 2
+        b = i % NBUF
         lo, hi = i * P, min(n, (i + 1) * P)
         k = hi - lo
         k0, k1 = lo // c, -(-hi // c)
         o0, o1 = int(prefix[k0]), int(prefix[k1])
         with torch.cuda.stream(st.h2d):
-            if i >= 2:
+            if i >= NBUF:
                 st.h2d.wait_event(ev_dec[b])
             c0, c1 = packed_nbytes(lo, cb), packed_nbytes(hi, cb)
             codes_d[b][:c1 - c0].copy_(codes_h[c0:c1], non_blocking=True)
@@ -202,7 +203,7 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
             cnt_d[b][:k1 - k0].copy_(counts_h[k0:k1], non_blocking=True)
             ev_h2d[b].record(st.h2d)
         st.comp.wait_event(ev_h2d[b])
-        if i >= 2:
+        if i >= NBUF:
             st.comp.wait_event(ev_d2h[b])
         src = N.SzEncodedIn()
         src.d_codes, src.d_sm = N.ptr(codes_d[b]), N.ptr(sm_d[b])
