@@ -408,11 +408,13 @@ def _raise_from_status(raw: np.ndarray, streams: EncodedStreams, config: CodecCo
                        codebook: ExponentCodebook, values_dev: torch.Tensor | None) -> None:
     st, first = _status_view(raw)
     flags = st.flags
-    if (config.chunked and flags & (1 << N.DEC_COUNTS_TOTAL) and values_dev is not None
-            and streams.n_escapes):
+    inconsistent = ((config.chunked and flags & (1 << N.DEC_COUNTS_TOTAL)) or
+                    (config.sentinel and flags & (1 << N.DEC_SENTINEL_COUNT)))
+    if inconsistent and values_dev is not None and streams.n_escapes:
         # The fused kernel checks escape values only for ordinals its tiles
-        # visit; with inconsistent counts some are never visited, and the
-        # reference checks values first (codec.py:446-457) — complete them.
+        # visit; with inconsistent counts (or sentinel marks) some are never
+        # visited, and the reference checks values first (codec.py:446-457)
+        # — complete them.
         full = _check_values_device(values_dev, int(streams.n_escapes), config, codebook)
         first[N.DEC_VALUE_DOMAIN] = full[N.DEC_VALUE_DOMAIN]
         first[N.DEC_VALUE_IN_BOOK] = full[N.DEC_VALUE_IN_BOOK]

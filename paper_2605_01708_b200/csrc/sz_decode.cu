@@ -37,6 +37,7 @@ struct OffsetsArgs {
   unsigned long long* tile_counter;
   uint64_t num_tiles;
   sz_decode_status* status;
+  int32_t sentinel;       // counts are per-tile sentinel marks (codec.py:459-467)
 };
 
 // counts per thread: 64 -> 16384 chunks per CTA, so the look-back chain of
@@ -100,9 +101,99 @@ __global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) 
   }
   if (tile == a.num_tiles - 1 && tid == 0) {
     a.offsets[a.n_counts] = s_total;
-    a.status->counts_total = s_total;
     const uint64_t m = a.m_ptr ? *a.m_ptr : a.m;
-    if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_COUNTS_TOTAL);
+    if (a.sentinel) {
+      a.status->marks_total = s_total;
+      if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_SENTINEL_COUNT);
+    } else {
+      a.status->counts_total = s_total;
+      if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_COUNTS_TOTAL);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3s
+// Sentinel mode (codec.py:459-467): escapes are marked in-band by the top
+// code, so an escape's ordinal is the number of marks before it.  This pass
+// counts the marks of every decode tile (codes plane only, 0.5 B/element for
+// 4-bit codes); offsets_kernel scans the counts, and the persistent decoder's
+// stagers turn each tile's marks into the same bitmap / first-index / value
+// staging as explicit mode — no look-back inside the streaming kernel.
+template <int CB, int EPV>
+__device__ __forceinline__ uint32_t slot_marks(const uint32_t* cw, int nv) {
+  // per code: all CB bits set == the sentinel; marks are rare, so test the
+  // whole slot first and gather the flag bits only when one is present
+  uint32_t t[EPV * CB / 32 + 1];
+  uint32_t any = 0;
+  if constexpr (CB == 4) {
+#pragma unroll
+    for (int i = 0; i < EPV / 8; ++i) {
+      const uint32_t x = cw[i];
+      t[i] = x & (x >> 1) & (x >> 2) & (x >> 3) & 0x11111111u;  // nibble == 15
+      any |= t[i];
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < EPV / 4; ++g) {
+      const uint32_t v = group_bits<12>(cw, g);
+      const uint32_t f = v & (v >> 1) & (v >> 2) & 0x249u;         // code == 7
+      any |= f;
+      if (g % 2 == 0) t[g / 2] = f; else t[g / 2] |= f << 16;
+    }
+  }
+  if (!any) return 0u;
+  uint32_t mk = 0;
+  if constexpr (CB == 4) {
+#pragma unroll
+    for (int i = 0; i < EPV / 8; ++i) {   // bits 0,4,..,28 -> bits 0..7
+      uint32_t u = (t[i] | (t[i] >> 3)) & 0x03030303u;
+      u = (u | (u >> 6)) & 0x000F000Fu;
+      u = (u | (u >> 12)) & 0xFFu;
+      mk |= u << (8 * i);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPV / 8; ++i) {   // bits 0,3,6,9 (+16) -> bits 0..7
+      const uint32_t f = t[i];
+      const uint32_t u = (f & 1u) | ((f >> 2) & 2u) | ((f >> 4) & 4u) | ((f >> 6) & 8u) |
+                         ((f >> 12) & 16u) | ((f >> 14) & 32u) | ((f >> 16) & 64u) |
+                         ((f >> 18) & 128u);
+      mk |= u << (8 * i);
+    }
+  }
+  if (nv < EPV) mk &= (1u << nv) - 1u;
+  return mk;
+}
+
+template <int FMT, int CB>
+__global__ void __launch_bounds__(kThreads)
+    marks_kernel(const uint8_t* __restrict__ codes, uint64_t n, uint64_t codes_len,
+                 uint64_t num_tiles, uint32_t tile_slots, uint32_t* __restrict__ tile_marks) {
+  constexpr int EPV = kEpv<FMT>;
+  constexpr int CBYTES = EPV * CB / 8;
+  constexpr int CWORDS = (CBYTES + 3) / 4;
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t t = gw; t < num_tiles; t += nw) {   // one warp per tile
+    uint32_t cnt = 0;
+    for (uint32_t j = lane; j < tile_slots; j += 32) {
+      const uint64_t e0 = (t * tile_slots + j) * EPV;
+      if (e0 >= n) break;
+      const int nv = e0 + EPV <= n ? EPV : static_cast<int>(n - e0);
+      uint32_t cw[CWORDS];
+      if (nv == EPV && !(CBYTES & 3)) {
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(codes + e0 * CB / 8);
+#pragma unroll
+        for (int i = 0; i < CWORDS; ++i) cw[i] = __ldg(q + i);
+      } else {
+        ld_bytes_clipped<CBYTES>(codes, e0 * CB / 8, cw, codes_len);
+      }
+      cnt += __popc(slot_marks<CB, EPV>(cw, nv));
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if (lane == 0) tile_marks[t] = cnt;
   }
 }
 
@@ -229,270 +320,6 @@ __device__ uint64_t warp_lower_bound(const uint32_t* pos, uint64_t m, uint64_t t
   return lo + __popc(__ballot_sync(0xffffffffu, less));
 }
 
-template <int FMT, int CB, int POSB, int ITEMS>
-__global__ void __launch_bounds__(kThreads)
-    decode_kernel(const __grid_constant__ sz_params p, const DecodeArgs a) {
-  constexpr int EPV = kEpv<FMT>;
-  constexpr int G = EPV / 4;
-  constexpr int WB = Fmt<FMT>::kWordBytes;
-  constexpr int SMB = Fmt<FMT>::kSmBits;
-  constexpr int CBYTES = EPV * CB / 8;
-  constexpr int SBYTES = EPV * SMB / 8;
-  constexpr int CWORDS = (CBYTES + 3) / 4;
-  constexpr int SWORDS = (SBYTES + 3) / 4;
-  constexpr int SLOTS = ITEMS * kThreads;
-  constexpr uint64_t TILE = static_cast<uint64_t>(SLOTS) * EPV;
-  constexpr bool SENT = POSB == 0;
-  constexpr bool ABS = POSB == 4;
-  constexpr int LUT2 = CB == 4 ? 256 : 64;
-  constexpr int kOffStage = 1024;
-
-  // pair LUT: byte0/1 = exponents of the two codes, byte2 bit0/1 = code out of
-  // range (not counting sentinel marks), byte3 bit0/1 = sentinel mark.
-  __shared__ uint32_t lut2[LUT2];
-  __shared__ uint32_t bitmap[SENT ? 1 : TILE / 32];
-  __shared__ uint8_t vals[SENT ? 4 : TILE];
-  __shared__ uint64_t s_off[SENT || ABS ? 1 : kOffStage + 1];
-  __shared__ BlockScanSmem<ITEMS> scan_sm;
-  __shared__ unsigned long long s_tile;
-  __shared__ uint64_t s_lo, s_hi, s_ka, s_excl;
-
-  const int tid = threadIdx.x;
-  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
-  constexpr uint32_t kCodeMask = (1u << CB) - 1;
-  const uint32_t sentinel_code = SENT ? kCodeMask : 0xFFu;
-  for (int i = tid; i < LUT2; i += kThreads) {
-    const uint32_t c0 = i & kCodeMask, c1 = (i >> CB) & kCodeMask;
-    const uint32_t mk0 = c0 == sentinel_code, mk1 = c1 == sentinel_code;
-    const uint32_t bad0 = !mk0 && c0 >= p.n_entries, bad1 = !mk1 && c1 >= p.n_entries;
-    lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | ((bad0 | (bad1 << 1)) << 16) |
-              ((mk0 | (mk1 << 1)) << 24);
-  }
-  if (tid == 0) s_tile = SENT ? atomicAdd(a.tile_counter, 1ull) : blockIdx.x;
-  if constexpr (!SENT) {
-    for (int i = tid; i < static_cast<int>(TILE / 32); i += kThreads) bitmap[i] = 0;
-  }
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t s = tile * TILE;
-  const uint64_t e = min(s + TILE, n);
-
-  // ---- loads of both planes for all items
-  uint32_t cw[ITEMS][CWORDS], sw[ITEMS][SWORDS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint64_t e0 = s + static_cast<uint64_t>(i * kThreads + tid) * EPV;
-    const uint64_t coff = e0 * CB / 8, soff = e0 * SMB / 8;
-    if (e0 + EPV <= n) {
-      ld_packed<CBYTES>(a.codes + coff, cw[i]);
-      ld_packed<SBYTES>(a.sm + soff, sw[i]);
-    } else {
-      ld_bytes_clipped<CBYTES>(a.codes, coff, cw[i], e0 < n ? a.codes_len : 0);
-      ld_bytes_clipped<SBYTES>(a.sm, soff, sw[i], e0 < n ? a.sm_len : 0);
-    }
-  }
-
-  // ---- distributed per-ordinal checks (independent of the chunk counts)
-  {
-    const uint64_t q = (m + a.num_tiles - 1) / a.num_tiles;
-    const uint64_t o0 = tile * q, o1 = min(o0 + q, m);
-    const uint32_t exp_bins = 1u << Fmt<FMT>::kExpBits;
-    for (uint64_t o = o0 + tid; o < o1; o += kThreads) {
-      const uint32_t v = a.values[o];
-      if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-      else if (!(p.enc_lut[v] & 0x10)) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-      if constexpr (ABS) {
-        const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
-        const uint32_t pv = pos[o];
-        if (pv >= n) record_first(&a.status->first_inv[SZ_DEC_ABS_PAST_END], o);
-        if (o > 0 && pv <= pos[o - 1]) record_first(&a.status->first_inv[SZ_DEC_ABS_NOT_INC], o);
-      }
-    }
-  }
-
-  // ---- pad-bit checks on the final bytes (codec.py:441-442, 236-237)
-  if (tile == a.num_tiles - 1 && tid == 0) {
-    const uint32_t cbits = static_cast<uint32_t>((n * CB) & 7);
-    if (cbits && (a.codes[a.codes_len - 1] >> cbits)) record_first(&a.status->first_inv[SZ_DEC_CODE_PAD], 0);
-    if constexpr (SMB != 8) {
-      const uint32_t sbits = static_cast<uint32_t>((n * SMB) & 7);
-      if (sbits && (a.sm[a.sm_len - 1] >> sbits)) record_first(&a.status->first_inv[SZ_DEC_SM_PAD], 0);
-    }
-  }
-
-  // ---- stage this tile's escapes (explicit modes)
-  if constexpr (!SENT) {
-    if constexpr (ABS) {
-      if (tid < 32) {
-        const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
-        const uint64_t lo = warp_lower_bound(pos, m, s);
-        const uint64_t hi = warp_lower_bound(pos, m, e);
-        if (tid == 0) { s_lo = lo; s_hi = max(hi, lo); }
-      }
-      __syncthreads();
-      const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
-      for (uint64_t o = s_lo + tid; o < s_hi; o += kThreads) {
-        const uint64_t idx = pos[o];
-        if (idx >= s && idx < e) {
-          const uint32_t rel = static_cast<uint32_t>(idx - s);
-          atomicOr(&bitmap[rel >> 5], 1u << (rel & 31));
-          vals[rel] = a.values[o];
-        }
-      }
-    } else {
-      const uint64_t ka = s / a.chunk, kb = (e - 1) / a.chunk;
-      const uint64_t nk = kb - ka + 2;   // offsets ka..kb+1
-      const bool staged = nk <= kOffStage + 1;
-      if (staged)
-        for (uint64_t i = tid; i < nk; i += kThreads) s_off[i] = a.offsets[ka + i];
-      if (tid == 0) {
-        s_ka = ka;
-        s_lo = min(a.offsets[ka], m);
-        s_hi = min(a.offsets[kb + 1], m);
-      }
-      __syncthreads();
-      const uint64_t* off = staged ? s_off : a.offsets + ka;
-      for (uint64_t o = s_lo + tid; o < s_hi; o += kThreads) {
-        // chunk of ordinal o: last k in [0, nk-1) with off[k] <= o
-        uint64_t lo = 0, hi = nk - 1;
-        while (hi - lo > 1) {
-          const uint64_t mid = (lo + hi) >> 1;
-          if (off[mid] <= o) lo = mid; else hi = mid;
-        }
-        const uint64_t k = ka + lo;
-        const uint64_t pv = load_pos<POSB>(a.positions, o);
-        if (pv >= a.chunk) {
-          record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
-          continue;
-        }
-        const uint64_t idx = k * a.chunk + pv;
-        if (idx >= n) {
-          record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
-          continue;
-        }
-        if (o > off[lo] && load_pos<POSB>(a.positions, o - 1) >= pv)
-          record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
-        if (idx >= s && idx < e) {
-          const uint32_t rel = static_cast<uint32_t>(idx - s);
-          atomicOr(&bitmap[rel >> 5], 1u << (rel & 31));
-          vals[rel] = a.values[o];
-        }
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---- dense decode: pair-LUT exponents, flags
-  uint32_t eg[ITEMS][G], ag[ITEMS][G];
-  uint32_t marks[ITEMS];
-  uint32_t cnt[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint64_t e0 = s + static_cast<uint64_t>(i * kThreads + tid) * EPV;
-    const int nv = e0 + EPV <= n ? EPV : (e0 < n ? static_cast<int>(n - e0) : 0);
-    uint32_t bad = 0, mk = 0;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      uint32_t l0, l1;
-      if constexpr (CB == 4) {
-        const uint32_t cb16 = group_bits<16>(cw[i], g);
-        l0 = lut2[cb16 & 0xFF];
-        l1 = lut2[cb16 >> 8];
-      } else {
-        const uint32_t cb12 = group_bits<12>(cw[i], g);
-        l0 = lut2[cb12 & 0x3F];
-        l1 = lut2[cb12 >> 6];
-      }
-      eg[i][g] = __byte_perm(l0, l1, 0x5410);
-      const uint32_t v = min(max(nv - 4 * g, 0), 4);
-      const uint32_t vmask = (1u << v) - 1u;
-      bad |= ((((l0 >> 16) & 3) | (((l1 >> 16) & 3) << 2)) & vmask) << (4 * g);
-      if constexpr (SENT) mk |= ((((l0 >> 24) & 3) | (((l1 >> 24) & 3) << 2)) & vmask) << (4 * g);
-      if constexpr (SMB == 8) ag[i][g] = sw[i][g];
-      else if constexpr (SMB == 4) ag[i][g] = unpack_nib4(group_bits<16>(sw[i], g));
-      else ag[i][g] = unpack_tri4(group_bits<12>(sw[i], g));
-    }
-    if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
-    marks[i] = mk;
-    cnt[i] = __popc(mk);
-  }
-
-  if constexpr (SENT) {
-    // ordinal of each marked element: block scan + look-back over mark counts
-    uint32_t excl[ITEMS];
-    const uint32_t total = block_scan<ITEMS>(cnt, excl, scan_sm);
-    if (tid < 32) {
-      const uint64_t ex = lookback_warp(a.states, tile, total);
-      if (tid == 0) {
-        s_excl = ex;
-        if (tile == a.num_tiles - 1) {
-          a.status->marks_total = ex + total;
-          if (ex + total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_SENTINEL_COUNT);
-        }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t mk = marks[i];
-      if (!mk) continue;
-      uint64_t ord = s_excl + excl[i];
-      // fully unrolled over (group, byte) so eg stays in registers
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if ((mk >> (4 * g + b)) & 1u) {
-            const uint32_t v = ord < m ? a.values[ord] : 0u;
-            ++ord;
-            eg[i][g] = (eg[i][g] & ~(0xFFu << (8 * b))) | (v << (8 * b));
-          }
-        }
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const uint32_t slot = i * kThreads + tid;
-      uint32_t bm;
-      if constexpr (EPV == 32) bm = bitmap[slot];
-      else bm = (bitmap[slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
-      if (!bm) continue;
-      const uint64_t e0 = s + static_cast<uint64_t>(slot) * EPV;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          constexpr int kDummy = 0;
-          const int j = 4 * g + b;
-          if ((bm >> j) & 1u) {
-            uint32_t code;
-            if constexpr (CB == 4) code = (cw[i][j >> 3] >> (4 * (j & 7))) & 0xF;
-            else code = (group_bits<12>(cw[i], g) >> (3 * b)) & 7;
-            if (code != kDummy) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-            const uint32_t v = vals[slot * EPV + j];
-            eg[i][g] = (eg[i][g] & ~(0xFFu << (8 * b))) | (v << (8 * b));
-          }
-        }
-      }
-    }
-  }
-
-  // ---- rebuild words and store
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const uint64_t e0 = s + static_cast<uint64_t>(i * kThreads + tid) * EPV;
-    uint32_t ow[8];
-#pragma unroll
-    for (int g = 0; g < G; ++g) rebuild_group<FMT>(eg[i][g], ag[i][g], ow, g);
-    if (e0 + EPV <= n) {
-      st256(out_slot<WB>(a, e0), ow);
-    } else if (e0 < n) {
-      st_bytes_clipped<32>(a.out, e0 * WB, ow, n * WB);
-    }
-  }
-}
-
 // ------------------------------------------------------------------ K4 (persistent)
 // Explicit modes (chunk-relative and abs32).  Same warp-specialised shape as
 // the encoder: warp 8 streams each tile's code and sign|mantissa planes into a
@@ -538,6 +365,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   constexpr int SWORDS = (SBYTES + 3) / 4;
   constexpr uint64_t TILE = static_cast<uint64_t>(kDecSlots) * EPV;
   constexpr bool ABS = POSB == 4;
+  constexpr bool SENT = POSB == 0;   // sentinel mode: marks in the code plane
   constexpr int LUT2 = CB == 4 ? 256 : 64;
   constexpr uint32_t kCodeMask = (1u << CB) - 1;
   using Smem = DecSmem<FMT>;
@@ -627,10 +455,12 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       // Direct happens-before with the decode warps' last use of this stage
       // (already guaranteed through the producer's chain; free to re-check).
       mbar_wait(&S.empty[s], ph ^ 1);
+      if constexpr (!SENT) {  // (sentinel staging writes every bitmap word itself)
 #pragma unroll
-      for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
+        for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
 #pragma unroll
-      for (int i = lane; i < kDecSlots; i += 32) S.slot_first[s][i] = kNoEscape;
+        for (int i = lane; i < kDecSlots; i += 32) S.slot_first[s][i] = kNoEscape;
+      }
       // Stage one in-tile escape: bitmap bit, slot's first compact index,
       // compact value (c = ordinal - first in-tile ordinal).
       auto stage = [&](uint64_t idx, uint64_t c, uint32_t v) {
@@ -667,7 +497,76 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
       }
       __syncwarp();
-      if constexpr (ABS) {
+      if constexpr (SENT) {
+        // Sentinel mode (codec.py:459-467): the tile's marks come from its
+        // code plane (landed in shared memory), its first ordinal from the
+        // K3s scan; the staging is then exactly explicit mode's.
+        mbar_wait(&S.full[s], ph);
+        const uint64_t t_first = a.offsets[tile];
+        const uint64_t t_end = max(a.offsets[tile + 1], t_first);
+        o_first = t_first;
+        const uint32_t full_slots = static_cast<uint32_t>(min(n - s0, TILE) / EPV);
+        const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
+        constexpr int SPL = kDecSlots / 32;  // consecutive slots per lane
+        uint32_t mk[SPL];
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+          const uint32_t slot = lane * SPL + j;
+          const uint64_t e0 = s0 + static_cast<uint64_t>(slot) * EPV;
+          const int nv = e0 >= n ? 0 : (e0 + EPV <= n ? EPV : static_cast<int>(n - e0));
+          uint32_t cw[CWORDS];
+          if ((slot + 1) * CBYTES <= cbytes) {
+            const uint8_t* cp = S.codes[s] + slot * CBYTES;
+            if constexpr (CBYTES == 16) {
+              const uint4 v = *reinterpret_cast<const uint4*>(cp);
+              cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
+            } else if constexpr (CBYTES == 8) {
+              const uint2 v = *reinterpret_cast<const uint2*>(cp);
+              cw[0] = v.x; cw[1] = v.y;
+            } else if constexpr (CBYTES == 12) {
+              const uint32_t* q = reinterpret_cast<const uint32_t*>(cp);
+              cw[0] = q[0]; cw[1] = q[1]; cw[2] = q[2];
+            } else {
+              const uint16_t* q = reinterpret_cast<const uint16_t*>(cp);
+              cw[0] = q[0] | (static_cast<uint32_t>(q[1]) << 16);
+              cw[1] = q[2];
+            }
+          } else {
+            ld_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, nv > 0 ? a.codes_len : 0);
+          }
+          mk[j] = nv > 0 ? slot_marks<CB, EPV>(cw, nv) : 0u;
+          cnt += __popc(mk[j]);
+        }
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += o;
+        }
+        uint32_t run = incl - cnt;
+#pragma unroll
+        for (int j = 0; j < SPL; ++j) {
+          const uint32_t slot = lane * SPL + j;
+          if (mk[j]) S.slot_first[s][slot] = run;
+          run += __popc(mk[j]);
+          if constexpr (EPV == 32) {
+            S.bitmap[s][slot] = mk[j];
+          } else if (j & 1) {
+            S.bitmap[s][slot >> 1] = mk[j - 1] | (mk[j] << 16);
+          }
+        }
+        // the tile's values: staged (first kDecValCap) and checked
+        // (codec.py:446-457) — every ordinal the marks reach
+        const uint64_t o_hi = min(t_end, m);
+        for (uint64_t o = t_first + lane; o < o_hi; o += 32) {
+          const uint32_t v = a.values[o];
+          if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+          else if (!(p.enc_lut[v] & 0x10))
+            record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+          if (o - t_first < kDecValCap) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
+        }
+      } else if constexpr (ABS) {
         const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
         const uint64_t lo = warp_lower_bound(pos, m, s0);
         const uint64_t hi = max(lo, warp_lower_bound(pos, m, s1));
@@ -830,6 +729,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             bad |= (((l0 >> 16) & 3) | (((l1 >> 16) & 3) << 2)) << (4 * g);
           }
         }
+        if constexpr (SENT) bad &= ~S.bitmap[s][slot];  // marks are not dense codes
         if (bad) {
           if (nv < 32) bad &= (1u << nv) - 1u;
           if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
@@ -840,7 +740,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           const int j = __ffs(bm) - 1;
           bm &= bm - 1;
           const uint32_t code = (pick<CWORDS>(cw, j >> 3) >> (4 * (j & 7))) & 0xF;
-          if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+          if (!SENT && code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
           const uint32_t v = escape_value(S.vals[s], S.slot_first[s][slot], bm0, j, ofirst, m,
                                           a.values);
           const int g = j >> 2, sh = 8 * (j & 3);
@@ -878,6 +778,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         else if constexpr (SMB == 4) ag[g] = unpack_nib4(group_bits<16>(sw, g));
         else ag[g] = unpack_tri4(group_bits<12>(sw, g));
       }
+      if constexpr (SENT) {  // marks are not dense codes
+        if constexpr (EPV == 32) bad &= ~S.bitmap[s][slot];
+        else bad &= ~((S.bitmap[s][slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu);
+      }
       if (bad) {
         if (nv < 32) bad &= (1u << nv) - 1u;
         if (bad) record_first(&a.status->first_inv[SZ_DEC_CODE_RANGE], e0 + (__ffs(bad) - 1));
@@ -900,7 +804,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           const uint64_t hi = pick<CWORDS>(cw, (bit >> 5) + 1);
           code = static_cast<uint32_t>(((hi << 32) | lo) >> (bit & 31)) & 7;
         }
-        if (code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+        if (!SENT && code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
         const uint32_t v = escape_value(S.vals[s], S.slot_first[s][slot], bm0, j, ofirst, m,
                                         a.values);
         const int g = j >> 2, sh = 8 * (j & 3);
@@ -951,6 +855,7 @@ struct DecodeWs {
   unsigned long long* off_counter;
   uint64_t* dec_states;
   unsigned long long* dec_counter;
+  uint32_t* tile_marks;  // sentinel: marks per decode tile
   size_t zero_bytes;  // prefix of the workspace that must be zeroed
   size_t total;
 };
@@ -958,9 +863,11 @@ struct DecodeWs {
 DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   DecodeWs w{};
   const bool chunked = !p->sentinel && !p->abs32;
-  const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size : 0;
-  const uint64_t otiles = chunked ? offsets_tiles(nchunks) : 0;
   const uint64_t dtiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
+  // scanned counts: per-chunk escape counts, or (sentinel) per-tile marks
+  const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size
+                                   : (p->sentinel ? dtiles : 0);
+  const uint64_t otiles = nchunks ? offsets_tiles(nchunks) : 0;
   uint64_t* b = static_cast<uint64_t*>(base);
   // zeroed region first: look-back states + counters
   w.off_states = b;
@@ -969,7 +876,9 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   w.dec_counter = reinterpret_cast<unsigned long long*>(b + otiles + 1 + dtiles);
   w.zero_bytes = (otiles + dtiles + 2) * sizeof(uint64_t);
   w.offsets = b + otiles + dtiles + 2;
-  w.total = w.zero_bytes + (chunked ? (nchunks + 1) * sizeof(uint64_t) : 0) + 256;
+  w.tile_marks = reinterpret_cast<uint32_t*>(w.offsets + (nchunks ? nchunks + 1 : 0));
+  w.total = w.zero_bytes + (nchunks ? (nchunks + 1) * sizeof(uint64_t) : 0) +
+            (p->sentinel ? dtiles * sizeof(uint32_t) : 0) + 256;
   return w;
 }
 
@@ -980,13 +889,6 @@ int sm_count() {
   return sms;
 }
 
-// Sentinel mode: one CTA per tile, ordinals by block scan + look-back.
-template <int FMT, int CB>
-cudaError_t launch_sentinel(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
-  decode_kernel<FMT, CB, 0, kDecodeItems>
-      <<<static_cast<unsigned>(a.num_tiles), kThreads, 0, s>>>(p, a);
-  return cudaGetLastError();
-}
 // Explicit modes: persistent warp-specialised kernel.
 template <int FMT, int CB, int POSB>
 cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
@@ -1005,7 +907,7 @@ cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStrea
 template <int FMT, int CB>
 cudaError_t dec_pos(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
   switch (posb) {
-    case 0: return launch_sentinel<FMT, CB>(p, a, s);
+    case 0: return launch_persistent<FMT, CB, 0>(p, a, s);
     case 1: return launch_persistent<FMT, CB, 1>(p, a, s);
     case 2: return launch_persistent<FMT, CB, 2>(p, a, s);
     default: return launch_persistent<FMT, CB, 4>(p, a, s);
@@ -1059,16 +961,37 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   if (e == cudaSuccess) e = cudaMemsetAsync(d_ws, 0, w.zero_bytes, s);
   if (e != cudaSuccess) return sz_record_cuda(e);
 
-  if (chunked) {
+  const uint64_t dtiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
+  if (p->sentinel) {
+    // K3s: marks per decode tile, then their scan (tile ordinal bases) below
+    const uint64_t want = (dtiles + kWarps - 1) / kWarps;  // one warp per tile
+    const unsigned g = static_cast<unsigned>(want < 148 * 16 ? want : 148 * 16);
+    const uint64_t clen = (n * p->code_bits + 7) / 8;
+    const uint32_t slots = kDecSlots;
+    const uint8_t* codes = static_cast<const uint8_t*>(in->d_codes);
+    switch (p->fmt * 2 + (p->code_bits == 4)) {
+      case 0: marks_kernel<SZ_BF16, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+      case 1: marks_kernel<SZ_BF16, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+      case 2: marks_kernel<SZ_E5M2, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+      case 3: marks_kernel<SZ_E5M2, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+      case 4: marks_kernel<SZ_E4M3, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+      default: marks_kernel<SZ_E4M3, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return sz_record_cuda(e);
+  }
+  if (chunked || p->sentinel) {
     OffsetsArgs oa{};
     oa.m_ptr = in->d_n_escapes;
-    oa.counts = in->d_counts;
-    oa.n_counts = nchunks;
+    oa.counts = p->sentinel ? w.tile_marks : in->d_counts;
+    oa.sentinel = p->sentinel ? 1 : 0;
+    const uint64_t ncounts = p->sentinel ? dtiles : nchunks;
+    oa.n_counts = ncounts;
     oa.m = m;
     oa.offsets = w.offsets;
     oa.states = w.off_states;
     oa.tile_counter = w.off_counter;
-    oa.num_tiles = offsets_tiles(nchunks);
+    oa.num_tiles = offsets_tiles(ncounts);
     oa.status = d_status;
     offsets_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(oa);
     e = cudaGetLastError();

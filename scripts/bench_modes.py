@@ -1,0 +1,102 @@
+"""Codec-mode and chunk-size sweep on one B200 (BASELINE.json config 2's
+"encode/decode throughput sweep over chunk size", plus the ablation modes of
+the paper: top-8 3-bit, top-15 sentinel, abs32 positions, FP8 E5M2 / E4M3).
+
+Input: 2^31 words of the Llama-3.1-8B KV shape (32 layers x K/V x 32K tokens
+x 8 heads x 128), synthetic with the reference profile (in-book 0.72^i, 8
+escape values at eps = 0.16% for 4-bit top-16 books; top-8 books escape
+whatever the profile puts outside them).  Device time: CUDA events, 3 warm-up
++ 5 timed round trips, bitwise verified first.  One JSON line per config.
+"""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+import paper_2605_01708_b200 as sz  # noqa: E402
+from paper_2605_01708_b200.engine import DeviceCodec, synth_kv  # noqa: E402
+
+N = 1 << 31
+PAPER_H200 = {  # PAPER.md rows (H200) for the same modes, encode/decode GB/s
+    "bf16 top16 explicit c1024": (613.3, 2181.8),
+    "bf16 top8 3-bit c1024": (440.1, 710.5),
+    "bf16 top15 sentinel c1024": (396.0, 620.8),
+    "bf16 top16 explicit c256": (351.3, None),
+    "bf16 top16 abs32": (None, 1421.7),
+    "e5m2 top16 explicit c1024": (249.7, 564.9),
+    "e5m2 top8 3-bit c1024": (221.6, 340.8),
+    "e4m3 top8 3-bit c1024": (219.6, 366.9),
+}
+
+
+def profile(fmt):
+    if fmt is sz.ElementFormat.BF16:
+        return tuple((0x70 + i, 0.72 ** i) for i in range(16)), tuple(range(0x10, 0x18))
+    if fmt is sz.ElementFormat.FP8_E5M2:
+        return tuple((8 + i, 0.72 ** i) for i in range(16)), (0, 1, 2, 3, 28, 29, 30, 31)
+    return tuple((4 + i, 0.72 ** i) for i in range(8)), (0, 1, 2, 3, 12, 13, 14, 15)
+
+
+def run(name, fmt, words, k, bits, mode, chunk, pos):
+    bw, _ = profile(fmt)
+    entries = tuple(e for e, _ in bw)[:k]
+    book = sz.ExponentCodebook(fmt, entries, bits, mode)
+    cfg = sz.CodecConfig(fmt, bits, mode, chunk, pos, book)
+    eng = DeviceCodec(cfg, book, words.numel())
+    m = eng.ensure_capacity(words)
+    eng.decode()
+    eng.check_status()
+    assert int(eng.compare(words, eng.out)[0].item()) == 0, name
+    for _ in range(3):
+        eng.encode(words)
+        eng.decode()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    enc_ms = dec_ms = 0.0
+    for _ in range(5):
+        ev[0].record()
+        eng.encode(words)
+        ev[1].record()
+        eng.decode()
+        ev[2].record()
+        torch.cuda.synchronize()
+        enc_ms += ev[0].elapsed_time(ev[1])
+        dec_ms += ev[1].elapsed_time(ev[2])
+    raw = words.numel() * fmt.word_nbytes
+    payload = eng.payload_nbytes(m)
+    res = {"config": name, "escape_rate": round(m / words.numel(), 5),
+           "encode_gbs": round(raw * 5 / (enc_ms / 1e3) / 1e9, 1),
+           "decode_gbs": round(raw * 5 / (dec_ms / 1e3) / 1e9, 1),
+           "payload_ratio": round(raw / payload, 5)}
+    if name in PAPER_H200:
+        res["paper_h200_enc_dec"] = PAPER_H200[name]
+    print(json.dumps(res), flush=True)
+    del eng
+    torch.cuda.empty_cache()
+
+
+def main():
+    E, S = sz.CodebookMode.TOPK_EXPLICIT, sz.CodebookMode.TOP15_SENTINEL
+    C, A = sz.PositionMode.CHUNK_RELATIVE, sz.PositionMode.ABSOLUTE_32
+    for fmt in (sz.ElementFormat.BF16, sz.ElementFormat.FP8_E5M2, sz.ElementFormat.FP8_E4M3):
+        bw, esc = profile(fmt)
+        words = synth_kv(N, fmt, 17, bw, esc, 0.0016)
+        f = fmt.cli_name
+        if fmt is sz.ElementFormat.FP8_E4M3:
+            run(f"{f} top8 3-bit c1024", fmt, words, 8, 3, E, 1024, C)
+        else:
+            run(f"{f} top16 explicit c1024", fmt, words, 16, 4, E, 1024, C)
+            run(f"{f} top8 3-bit c1024", fmt, words, 8, 3, E, 1024, C)
+        if fmt is sz.ElementFormat.BF16:
+            run(f"{f} top15 sentinel c1024", fmt, words, 15, 4, S, 1024, C)
+            run(f"{f} top16 abs32", fmt, words, 16, 4, E, 1024, A)
+            for c in (256, 2048, 4096, 16384, 65536):
+                run(f"{f} top16 explicit c{c}", fmt, words, 16, 4, E, c, C)
+        del words
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
