@@ -501,10 +501,23 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         // Sentinel mode (codec.py:459-467): the tile's marks come from its
         // code plane (landed in shared memory), its first ordinal from the
         // K3s scan; the staging is then exactly explicit mode's.
-        mbar_wait(&S.full[s], ph);
         const uint64_t t_first = a.offsets[tile];
         const uint64_t t_end = max(a.offsets[tile + 1], t_first);
         o_first = t_first;
+        {
+          // the tile's values first — staged (first kDecValCap) and checked
+          // (codec.py:446-457) for every ordinal its marks reach — while its
+          // code plane is still in flight
+          const uint64_t o_hi = min(t_end, m);
+          for (uint64_t o = t_first + lane; o < o_hi; o += 32) {
+            const uint32_t v = a.values[o];
+            if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+            else if (!(p.enc_lut[v] & 0x10))
+              record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+            if (o - t_first < kDecValCap) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
+          }
+        }
+        mbar_wait(&S.full[s], ph);
         const uint32_t full_slots = static_cast<uint32_t>(min(n - s0, TILE) / EPV);
         const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
         constexpr int SPL = kDecSlots / 32;  // consecutive slots per lane
@@ -555,16 +568,6 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           } else if (j & 1) {
             S.bitmap[s][slot >> 1] = mk[j - 1] | (mk[j] << 16);
           }
-        }
-        // the tile's values: staged (first kDecValCap) and checked
-        // (codec.py:446-457) — every ordinal the marks reach
-        const uint64_t o_hi = min(t_end, m);
-        for (uint64_t o = t_first + lane; o < o_hi; o += 32) {
-          const uint32_t v = a.values[o];
-          if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-          else if (!(p.enc_lut[v] & 0x10))
-            record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-          if (o - t_first < kDecValCap) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
         }
       } else if constexpr (ABS) {
         const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
