@@ -26,3 +26,22 @@ for fmt_id, fmt, bk, esc in ((0, sz.ElementFormat.BF16, O.BF16_BOOK, O.BF16_ESC)
         sz.build_histogram(st)
 torch.cuda.synchronize()
 print("sanitize ok")
+
+# paged KV (segments) and device container framing
+from paper_2605_01708_b200 import container, paged  # noqa: E402
+from paper_2605_01708_b200.engine import synth_kv  # noqa: E402
+for fmt, bk, esc in ((sz.ElementFormat.BF16, O.BF16_BOOK, O.BF16_ESC),
+                     (sz.ElementFormat.FP8_E5M2, O.E5M2_BOOK, O.E5M2_ESC)):
+    book = sz.ExponentCodebook(fmt, tuple(e for e, _ in bk), 4, sz.CodebookMode.TOPK_EXPLICIT)
+    cfg = sz.CodecConfig(fmt, codebook=book)
+    caches = [synth_kv(24 * 2 * 16 * 2 * 64, fmt, 9 + l, bk, esc, 0.05).view(24, 2, 16, 2, 64)
+              for l in range(2)]
+    ids = torch.randperm(24)[:11].cuda()
+    enc = paged.encode_kv_blocks(caches, ids, cfg)
+    dst = [torch.zeros_like(c) for c in caches]
+    paged.decode_kv_blocks(enc, cfg, book, dst, ids.flip(0))
+    words = synth_kv(70_001, fmt, 3, bk, esc, 0.01)
+    buf = container.encode_container(sz.RawTensorStream(fmt, words), cfg)
+    assert torch.equal(container.decode_container(buf).words, words)
+torch.cuda.synchronize()
+print("sanitize paged+container ok")
