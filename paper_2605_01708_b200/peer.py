@@ -274,9 +274,9 @@ def connect_pair(role: str, peer: int, piece: int, config: CodecConfig,
     Teardown: ``close()`` on both ends (unmaps the peer's region), a
     barrier, then ``release()`` on both (frees the own region).
     """
-    dev = N.device()
     if piece % config.chunk_size and config.chunked:
         raise ValueError("piece must be a multiple of the chunk size")
+    dev = N.device()
     _preload(config, codebook, dev)
     lay = SlotLayout(piece, config, slots)
     if loopback:
