@@ -733,6 +733,7 @@ struct GatherArgs {
   uint32_t* heavy_list;
   uint64_t* heavy_pref;           // per listed tile: first global ordinal
   unsigned int* heavy_count;
+  uint32_t split;                 // CTAs per group (record moves split R ways)
 };
 
 // Tiles per CTA: 256 (8 per lane in the scan) keeps the look-back chain
@@ -752,9 +753,14 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ uint8_t lut[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int i = tid; i < 256; i += kThreads) lut[i] = p.enc_lut[i];
+  // Tickets in launch order: group = ticket / R, part = ticket % R.  Part 0
+  // runs the decoupled look-back and publishes; parts 1..R-1 only read the
+  // predecessors' states (earlier tickets: forward progress) and move their
+  // slice of the group's records — escape-dense inputs get R x the CTAs.
   if (tid == 0) s_group = atomicAdd(a.counter, 1ull);
   __syncthreads();
-  const uint64_t group = s_group;
+  const uint64_t group = s_group / a.split;
+  const uint32_t part = static_cast<uint32_t>(s_group % a.split);
   const uint64_t t0 = group * kGatherTiles;
   if (warp == 0) {
     // each lane owns kTilesPerLane consecutive tiles of the group
@@ -774,7 +780,8 @@ __global__ void __launch_bounds__(kThreads)
       if (lane >= d) incl += o;
     }
     const uint64_t agg = __shfl_sync(0xffffffffu, incl, 31);
-    const uint64_t ex = lookback_warp(a.states, group, agg);
+    const uint64_t ex = part == 0 ? lookback_warp(a.states, group, agg)
+                                  : (group ? lookback_wide<8>(a.states, group) : 0);
     const uint64_t base = *a.base_snapshot;
     uint64_t run = base + ex + incl - lsum;
 #pragma unroll
@@ -783,7 +790,7 @@ __global__ void __launch_bounds__(kThreads)
       tcnt[lane * kTilesPerLane + j] = c[j];
       run += c[j];
     }
-    if (lane == 0 && group == a.num_groups - 1) {
+    if (lane == 0 && part == 0 && group == a.num_groups - 1) {
       *a.n_escapes = ex + agg;
       if (a.escape_base) *a.escape_base = base + ex + agg;
     }
@@ -793,8 +800,10 @@ __global__ void __launch_bounds__(kThreads)
   // records t, t+256, ... (tile found by a search over the 32 local prefixes),
   // so all loads of the group are in flight at once.
   {
-    const uint64_t g_base = tpref[0];
-    const uint64_t g_total = tpref[kGatherTiles - 1] + tcnt[kGatherTiles - 1] - g_base;
+    const uint64_t g_all = tpref[kGatherTiles - 1] + tcnt[kGatherTiles - 1] - tpref[0];
+    const uint64_t g_lo = g_all * part / a.split, g_hi = g_all * (part + 1) / a.split;
+    const uint64_t g_base = tpref[0] + g_lo;
+    const uint64_t g_total = g_hi - g_lo;
     // kGatherUnroll records per thread per round: all loads are issued before
     // any store, so the round costs one memory latency, not kGatherUnroll.
     constexpr int U = kGatherUnroll;
@@ -834,7 +843,7 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   // Escape-heavy tiles go to K2c (one CTA each, all of them in parallel).
-  if (warp == 0) {
+  if (warp == 0 && part == 0) {
 #pragma unroll
     for (int j = 0; j < kGatherTiles / 32; ++j) {
       const int k = j * 32 + lane;
@@ -1064,7 +1073,7 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
   kern<<<grid, kEncThreads, smem, s>>>(p, a, tm);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups), kThreads, 0, s>>>(p, g);
+  escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups * g.split), kThreads, 0, s>>>(p, g);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const uint64_t heavy_grid = want * 8;  // one wave of 256-thread CTAs
@@ -1206,6 +1215,9 @@ int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shi
   g.base_snapshot = w.snapshot;
   g.escape_base = out->d_escape_base;
   g.heavy_list = w.heavy_list;
+  // CTAs per group: enough for one wave of record movers on small inputs
+  // (few groups), one per group on large ones
+  g.split = static_cast<uint32_t>(g.num_groups >= 512 ? 1 : (g.num_groups >= 64 ? 4 : 16));
   g.heavy_pref = w.heavy_pref;
   g.heavy_count = w.heavy_count;
 
