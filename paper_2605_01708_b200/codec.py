@@ -505,7 +505,7 @@ def decode(streams: EncodedStreams, config: CodecConfig,
         from . import hostpipe
         if hostpipe.pipelinable(config, n):
             counts_np = to_numpy(streams.chunk_counts)
-            if int(counts_np.astype(np.int64).sum()) == m:
+            if int(counts_np.sum(dtype=np.int64)) == m:
                 out_h = hostpipe.decode_host(streams, config, codebook, counts_np)
                 if out_h is not None:
                     keep_torch = isinstance(streams.packed_codes, torch.Tensor)

@@ -136,8 +136,12 @@ def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCo
     m = int(base_d.cpu().numpy()[0])
     if m > cap:  # overflow protocol: rerun with the exact escape count
         return encode_host(words_h, config, codebook, capacity=m)
-    positions = pos_d[:m].to("cpu")
-    values = val_d[:m].to("cpu")
+    # escape sections into pinned memory too: the decode of these host
+    # sections then copies them back asynchronously
+    positions = torch.empty(m, dtype=pos_d.dtype, pin_memory=True)
+    positions.copy_(pos_d[:m])
+    values = torch.empty(m, dtype=torch.uint8, pin_memory=True)
+    values.copy_(val_d[:m])
     vp = None
     if fmt.exp_bits != 8:
         vp = pack_bits_device(val_d[:m], fmt.exp_bits).to("cpu")
@@ -162,9 +166,18 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     codes_h = host_tensor(streams.packed_codes, torch.uint8)
     sm_h = host_tensor(streams.sign_mantissa, torch.uint8)
     # small metadata: pinned so the H2D stream never blocks the host thread
-    counts_h = host_tensor(counts_np.astype(np.uint32, copy=False), torch.uint32).pin_memory()
-    # ordinal offset of every piece = escapes in the chunks before it
-    prefix = np.concatenate([[0], np.cumsum(counts_np.astype(np.int64))])
+    # (sections from encode_host already are)
+    cc = streams.chunk_counts
+    if isinstance(cc, torch.Tensor) and cc.is_pinned():
+        counts_h = cc.reshape(-1).view(torch.uint32)
+    else:
+        counts_h = host_tensor(counts_np.astype(np.uint32, copy=False), torch.uint32).pin_memory()
+    # ordinal offset of every piece = escapes in the chunks before it: only
+    # the piece boundaries are needed (one reduceat, no full prefix array)
+    bounds = np.arange(0, n, P) // c
+    per_piece = np.add.reduceat(counts_np, bounds, dtype=np.int64) if counts_np.size else \
+        np.zeros(len(bounds), np.int64)
+    piece_first = np.concatenate([[0], np.cumsum(per_piece)])
     out_h = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
     codes_d = [torch.empty(packed_nbytes(P, cb), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
     sm_d = [torch.empty(config.sm_nbytes(P), dtype=torch.uint8, device=dev) for _ in range(NBUF)]
@@ -192,7 +205,7 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
         lo, hi = i * P, min(n, (i + 1) * P)
         k = hi - lo
         k0, k1 = lo // c, -(-hi // c)
-        o0, o1 = int(prefix[k0]), int(prefix[k1])
+        o0, o1 = int(piece_first[i]), int(piece_first[i + 1])
         with torch.cuda.stream(st.h2d):
             if i >= NBUF:
                 st.h2d.wait_event(ev_dec[b])
