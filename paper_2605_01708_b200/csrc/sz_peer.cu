@@ -41,6 +41,9 @@ __global__ void peer_signal_kernel(uint64_t* flag, uint64_t value) {
 
 __global__ void peer_wait_kernel(const uint64_t* flag, uint64_t value, uint64_t timeout_ns,
                                  uint32_t* timed_out) {
+  // after one timeout the link is broken: later waits return at once, so a
+  // lost peer costs one timeout, not one per piece
+  if (timed_out && *reinterpret_cast<volatile uint32_t*>(timed_out)) return;
   const uint64_t t0 = globaltimer_ns();
   while (ld_acquire_sys(flag) < value) {
     if (globaltimer_ns() - t0 > timeout_ns) {
