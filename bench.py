@@ -184,9 +184,16 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # SZ_BENCH_BACKEND=gloo: test mode for the N > 1 code path with every rank
+    # on one GPU (time-sliced, not a measurement); the driver uses NCCL
+    backend = os.environ.get("SZ_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(local % torch.cuda.device_count() if backend == "gloo" else local)
+    local = torch.cuda.current_device()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -363,7 +370,7 @@ def run_ours(args) -> None:
     }
 
     if world >= 2 and world % 2 == 0 and not args.no_handoff and wl["fmt_id"] == 0:
-        line["handoff"] = handoff_leg(rank, world)
+        line["handoff"] = handoff_leg(rank, world, raw_baseline=backend == "nccl")
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m)
@@ -374,7 +381,7 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def handoff_leg(rank: int, world: int) -> dict:
+def handoff_leg(rank: int, world: int, raw_baseline: bool = True) -> dict:
     """Config 5 at N >= 2: pairs (2i -> 2i+1) hand 2 GiB of BF16 KV over in
     64 MiB pieces — raw NCCL P2P vs the fused encode -> peer-store -> decode
     link (peer.py) — for realistic and escape-heavy exponent statistics.
@@ -387,7 +394,7 @@ def handoff_leg(rank: int, world: int) -> dict:
         from bench_handoff import handoff_bench
         gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=120))
         res = handoff_bench(1 << 30, 1 << 25, 3, False, rank, world, obj_group=gloo,
-                            timeout_s=20.0)
+                            timeout_s=20.0, raw_baseline=raw_baseline)
         res["pairs"] = world // 2
         res["unit"] = "GB/s of BF16 KV per pair (raw bytes / max device time over ranks)"
         return res
