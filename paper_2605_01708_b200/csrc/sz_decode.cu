@@ -332,7 +332,6 @@ constexpr int kDecSlots = kDecItems * kThreads;        // 512 slots per tile
 constexpr int kDecHelpers = 3;                          // escape-staging warps
 constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
 constexpr int kDecOffStage = 256;                       // staged chunk offsets per helper
-
 template <int FMT>
 struct DecSmem {
   static constexpr int STAGES = 5;
@@ -384,6 +383,16 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     s_lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
   const uint32_t lut2_base = smem_addr(s_lut2);
+  // In-book exponents as a 256-bit set in shared memory: the stagers' value
+  // checks index it by escape value (a divergent index into the kernel
+  // parameters' enc_lut would serialise the constant cache per distinct value).
+  __shared__ uint32_t s_inbook[8];
+  if (tid < 8) {
+    uint32_t w = 0;
+    for (int b = 0; b < 32; ++b) w |= ((p.enc_lut[tid * 32 + b] >> 4) & 1u) << b;
+    s_inbook[tid] = w;
+  }
+  auto in_book = [&](uint32_t v) { return (s_inbook[v >> 5] >> (v & 31)) & 1u; };
   // E5M2 with 4-bit codes: a pair table indexed by a code byte (elements
   // 2i, 2i+1) whose u16 entries hold both exponents already at their E5M2
   // bit positions (bits 2-6 of each byte) — reconstruct (formats.py:136-155)
@@ -479,7 +488,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         for (uint64_t o = o0 + lane; o < o1; o += 32) {
           const uint32_t v = a.values[o];
           if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-          else if (!(p.enc_lut[v] & 0x10))
+          else if (!in_book(v))
             record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
           const uint32_t pv = pos[o];
           if (pv >= n) record_first(&a.status->first_inv[SZ_DEC_ABS_PAST_END], o);
@@ -512,7 +521,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           for (uint64_t o = t_first + lane; o < o_hi; o += 32) {
             const uint32_t v = a.values[o];
             if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-            else if (!(p.enc_lut[v] & 0x10))
+            else if (!in_book(v))
               record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
             if (o - t_first < kDecValCap) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
           }
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             // per-ordinal value checks (codec.py:451-457); complete coverage when
             // sum(counts) != M is restored on the host (sz_check_values)
             if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-            else if (!(p.enc_lut[v] & 0x10))
+            else if (!in_book(v))
               record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
             uint64_t lo = 0, hi = nk - 1;
             while (hi - lo > 1) {
@@ -634,6 +643,81 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           if (hit && o >= o_first) stage(idx, o - o_first, v);
         };
         constexpr int U = 4;
+        const uint64_t n_o = o_hi - o_lo;
+        if (staged && n_o < (1ull << 31)) {
+          // Fast path: the tile's chunk starts as u32 ordinals relative to o_lo
+          // (in place of the staged u64 offsets), and each round finds its
+          // lanes' chunks from the previous round's: one broadcast compare
+          // when the round crosses at most one chunk start (escape-dense
+          // tiles), a short binary search otherwise.  All per-ordinal checks
+          // fold into one predicate; the rare failing ordinal takes the
+          // detailed path.
+          uint32_t* const srel = reinterpret_cast<uint32_t*>(soff);
+          // in place, 32 entries at a time: block j's u32 stores only overwrite
+          // u64 entries < 32j + 16, all read already
+          for (uint32_t j0 = 0; j0 < nk; j0 += 32) {
+            const uint32_t i = j0 + lane;
+            const uint64_t v = i < nk ? soff[i] : 0;
+            __syncwarp();
+            if (i < nk) srel[i] = static_cast<uint32_t>(min(v, m) - o_lo);
+            __syncwarp();
+          }
+          const uint32_t nch = static_cast<uint32_t>(nk - 1), no = static_cast<uint32_t>(n_o);
+          uint32_t cur = 0;  // srel[cur] <= the round's first ordinal
+          for (uint32_t b0 = 0; b0 < no; b0 += 32 * U) {
+            uint32_t pvs[U], vs[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t orl = b0 + 32 * u + lane;
+              pvs[u] = orl < no ? static_cast<uint32_t>(load_pos<POSB>(a.positions, o_lo + orl)) : 0u;
+              vs[u] = orl < no ? a.values[o_lo + orl] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const uint32_t br = b0 + 32 * u;
+              if (br >= no) break;
+              const uint32_t orl = br + lane, pv = pvs[u], v = vs[u];
+              const bool live = orl < no;
+              const uint32_t last = min(br + 31, no - 1);
+              uint32_t k;
+              if (cur + 2 > nch || srel[cur + 2] > last) {
+                k = cur + (cur + 1 < nch && srel[cur + 1] <= orl ? 1u : 0u);
+              } else {
+                uint32_t lo = cur, hi = nch;
+                while (hi - lo > 1) {
+                  const uint32_t mid = (lo + hi) >> 1;
+                  if (srel[mid] <= orl) lo = mid; else hi = mid;
+                }
+                k = lo;
+              }
+              cur = __shfl_sync(0xffffffffu, k, 31);
+              uint32_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
+              if (lane == 0) prev = static_cast<uint32_t>(carry);
+              carry = __shfl_sync(0xffffffffu, pv, 31);
+              const uint64_t idx = (ka + k) * a.chunk + pv;
+              const bool pos_ok = pv < a.chunk && idx < n;
+              const bool bad = live && (v >= exp_bins || !in_book(v) || !pos_ok ||
+                                        (orl > srel[k] && prev >= pv));
+              if (bad) {  // rare: the reference's checks in order (codec.py:446-536)
+                const uint64_t o = o_lo + orl;
+                if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+                else if (!in_book(v)) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+                if (pv >= a.chunk) record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+                else if (idx >= n) record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+                else if (orl > srel[k] && prev >= pv)
+                  record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+              }
+              const bool hit = live && pos_ok && idx >= s0 && idx < s1;
+              const uint32_t hb = __ballot_sync(0xffffffffu, hit);
+              if (!have_first && hb) {
+                o_first = o_lo + br + (__ffs(hb) - 1);
+                have_first = true;
+              }
+              const uint64_t o = o_lo + orl;
+              if (hit && o >= o_first) stage(idx, o - o_first, v);
+            }
+          }
+        } else {
         uint64_t base = o_lo;
         for (; base + 32 * U <= o_hi; base += 32 * U) {
           uint64_t pvs[U];
@@ -650,6 +734,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           const uint64_t o = base + lane;
           one(base, o < o_hi ? load_pos<POSB>(a.positions, o) : 0,
               o < o_hi ? a.values[o] : 0u);
+        }
         }
       }
       if (lane == 0) S.ofirst[s] = o_first;

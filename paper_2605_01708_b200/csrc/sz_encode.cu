@@ -85,18 +85,30 @@ struct EncSmem {
   // 1024-aligned: the 128B-swizzle pattern of tensor TMA is a function of
   // shared-address bits 7-9
   alignas(1024) uint8_t in[kEncInStages][kEncTileBytes];
-  uint32_t fmask[kEncScanSlots][kEncSlots];
+  uint32_t fmask[kEncScanSlots][kEncSlots];  // at fsw(slot)
   // escape records (tile-local element index | raw exponent << 16), in
   // arbitrary order; the writer warp derives each one's rank from fmask
   uint32_t esc_rec[kEncScanSlots][kEscCap];
   uint32_t esc_n[kEncScanSlots];
-  uint16_t slot_pref[kWriterWarps][kEncSlots];  // per-slot exclusive escape prefix
+  uint32_t slot_pref[kWriterWarps][kEncSlots];  // per-slot exclusive escape prefix, at fsw(slot)
   uint64_t meta[kEncScanSlots];      // tile id (~0 = end of work)
   uint64_t full[kEncInStages];       // producer -> dense (TMA bytes)
   uint64_t in_empty[kEncInStages];   // dense -> producer
   uint64_t computed[kEncScanSlots];  // dense -> writer
   uint64_t scan_empty[kEncScanSlots];// writer -> producer
 };
+
+// Shared-memory index of a slot's escape mask (and slot prefix).  Dense warps
+// write 32 consecutive slots per warp; writer lane L reads its own 32
+// consecutive slots L*32 + j, which in a linear layout all sit in one bank
+// (32-way conflicts).  XOR-ing bits 5-9 of the slot into bits 0-4
+// (bits 5-7 -> 2-4, bits 8-9 -> 0-1) makes both patterns conflict-free, and
+// keeps every aligned group of 4 slots together (permuted inside), so 16-byte
+// reads of 4 masks stay conflict-free across each 8-lane phase too.
+__device__ __forceinline__ uint32_t fsw_key(uint32_t row) {  // row = slot >> 5
+  return ((row & 7u) << 2) | ((row >> 3) & 3u);
+}
+__device__ __forceinline__ uint32_t fsw(uint32_t slot) { return slot ^ fsw_key(slot >> 5); }
 
 template <int FMT>
 __device__ __forceinline__ void split_group(const uint32_t (&x)[8], int g, uint32_t& e4,
@@ -576,7 +588,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
                                           stile + slot * SBYTES, a,
                                           tile_e0 + static_cast<uint64_t>(slot) * EPV);
         }
-        S.fmask[q][slot] = fm;
+        S.fmask[q][fsw(slot)] = fm;
         if (fm) {  // rare: append (element, raw exponent) records for the writer
           uint32_t r = atomicAdd(&S.esc_n[q], static_cast<uint32_t>(__popc(fm)));
           uint32_t f = fm;
@@ -606,7 +618,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   // ---------------------------------------------------------------- writer warps
   constexpr int SPL = kEncSlots / 32;  // 32 consecutive slots per lane
   const int ww = warp - kWriterWarp0;  // owns iterations it == ww (mod kWriterWarps)
-  uint16_t* sp = S.slot_pref[ww];
+  uint32_t* sp = S.slot_pref[ww];
+  const uint32_t key = fsw_key(lane);  // this lane's slots: lane*SPL + (j ^ key)
   long long t_wait = 0, t_work = 0;
   for (uint32_t it = ww;; it += kWriterWarps) {
     const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
@@ -618,11 +631,11 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     if (tile == ~0ull) break;
     const uint64_t tile_e0 = tile * TILE;
 
-    const uint32_t* fm = &S.fmask[q][lane * SPL];
+    const uint32_t* fm = &S.fmask[q][lane * SPL];  // slot lane*SPL + j at fm[j ^ key]
     uint32_t cnt = 0;
 #pragma unroll
-    for (int j = 0; j < SPL; j += 4) {
-      const uint4 v = *reinterpret_cast<const uint4*>(fm + j);
+    for (int j = 0; j < SPL; j += 4) {  // (4 masks of one aligned group, permuted)
+      const uint4 v = *reinterpret_cast<const uint4*>(fm + (j ^ (key & ~3u)));
       cnt += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
     }
     uint32_t incl = cnt;
@@ -650,7 +663,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         const uint32_t per_lane = SPL / spc;
         for (uint32_t c = 0; c < per_lane; ++c) {
           uint32_t sum = 0;
-          for (uint32_t j = c * spc; j < (c + 1) * spc; ++j) sum += __popc(fm[j]);
+          for (uint32_t j = c * spc; j < (c + 1) * spc; ++j) sum += __popc(fm[j ^ key]);
           const uint64_t k = k_base + lane * per_lane + c;
           if (k < a.n_chunks) a.counts[k] = sum;
         }
@@ -663,7 +676,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         if (lane == 0) atomicAdd(&a.counts[k0], total);
       } else {
         for (int j = 0; j < SPL; ++j) {
-          uint32_t m = fm[j];
+          uint32_t m = fm[j ^ key];
           const uint64_t e0 = tile_e0 + static_cast<uint64_t>(lane * SPL + j) * EPV;
           while (m) {
             const int b = __ffs(m) - 1;
@@ -679,8 +692,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     if (total && total <= kEscCap && n_rec == total) {
       uint32_t run = excl_lane;
       for (int j = 0; j < SPL; ++j) {
-        sp[lane * SPL + j] = static_cast<uint16_t>(run);
-        run += __popc(fm[j]);
+        sp[lane * SPL + (j ^ key)] = run;
+        run += __popc(fm[j ^ key]);
       }
       __syncwarp();
       uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
@@ -688,7 +701,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       for (uint32_t r = lane; r < n_rec; r += 32) {
         const uint32_t rec = S.esc_rec[q][r];
         const uint32_t local = rec & 0xFFFFu, slot = local / EPV, b = local % EPV;
-        const uint32_t rank = sp[slot] + __popc(S.fmask[q][slot] & ((1u << b) - 1u));
+        const uint32_t rank = sp[fsw(slot)] + __popc(S.fmask[q][fsw(slot)] & ((1u << b) - 1u));
         sval[rank] = static_cast<uint8_t>(rec >> 16);
         put_position<POSB>(spos, rank, tile_e0 + local, a.chunk, a.chunk_shift);
       }
@@ -749,6 +762,9 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int WB = Fmt<FMT>::kWordBytes;
   __shared__ uint64_t tpref[kGatherTiles];
   __shared__ uint32_t tcnt[kGatherTiles];
+  // group-relative prefix of the records K2b moves (regular tiles only; an
+  // escape-heavy tile counts 0 here, K2c writes its records)
+  __shared__ uint32_t rpref[kGatherTiles + 1];
   __shared__ unsigned long long s_group;
   __shared__ uint8_t lut[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -767,17 +783,30 @@ __global__ void __launch_bounds__(kThreads)
     constexpr int kTilesPerLane = kGatherTiles / 32;
     uint32_t c[kTilesPerLane];
     uint64_t lsum = 0;
+    uint32_t rsum = 0;
 #pragma unroll
     for (int j = 0; j < kTilesPerLane; ++j) {
       const uint64_t t = t0 + lane * kTilesPerLane + j;
       c[j] = t < a.num_tiles ? a.tile_esc[t] : 0u;
       lsum += c[j];
+      rsum += c[j] <= kEscCap ? c[j] : 0u;
     }
     uint64_t incl = lsum;
+    uint32_t rincl = rsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += o;
+      const uint32_t ro = __shfl_up_sync(0xffffffffu, rincl, d);
+      if (lane >= d) { incl += o; rincl += ro; }
+    }
+    {
+      uint32_t rrun = rincl - rsum;
+#pragma unroll
+      for (int j = 0; j < kTilesPerLane; ++j) {
+        rpref[lane * kTilesPerLane + j] = rrun;
+        rrun += c[j] <= kEscCap ? c[j] : 0u;
+      }
+      if (lane == 31) rpref[kGatherTiles] = rincl;
     }
     const uint64_t agg = __shfl_sync(0xffffffffu, incl, 31);
     const uint64_t ex = part == 0 ? lookback_warp(a.states, group, agg)
@@ -797,12 +826,13 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   // Flat pass over every record of the group's regular tiles: thread t moves
-  // records t, t+256, ... (tile found by a search over the 32 local prefixes),
-  // so all loads of the group are in flight at once.
+  // records t, t+256, ... (tile found by a search over the regular-record
+  // prefixes), so all loads of the group are in flight at once.  Heavy
+  // tiles' records are not visited at all (an all-heavy input leaves K2b
+  // only its scan and the listing).
   {
-    const uint64_t g_all = tpref[kGatherTiles - 1] + tcnt[kGatherTiles - 1] - tpref[0];
+    const uint64_t g_all = rpref[kGatherTiles];
     const uint64_t g_lo = g_all * part / a.split, g_hi = g_all * (part + 1) / a.split;
-    const uint64_t g_base = tpref[0] + g_lo;
     const uint64_t g_total = g_hi - g_lo;
     // kGatherUnroll records per thread per round: all loads are issued before
     // any store, so the round costs one memory latency, not kGatherUnroll.
@@ -813,16 +843,17 @@ __global__ void __launch_bounds__(kThreads)
       bool live[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t o = g_base + r0 + u * kThreads;
-        int lo = 0, hi = kGatherTiles;  // last k with tpref[k] <= o
+        const uint32_t r = static_cast<uint32_t>(g_lo + r0 + u * kThreads);
+        int lo = 0, hi = kGatherTiles;  // last k with rpref[k] <= r: r's tile
 #pragma unroll
         for (int step = 0; step < 8; ++step) {  // log2(kGatherTiles) halvings
           const int mid = (lo + hi) >> 1;
-          if (tpref[mid] <= o) lo = mid; else hi = mid;
+          if (rpref[mid] <= r) lo = mid; else hi = mid;
         }
-        live[u] = r0 + u * kThreads < g_total && tcnt[lo] <= kEscCap && o < a.capacity;
-        src[u] = (t0 + lo) * kEscCap + (o - tpref[lo]);
-        dst[u] = o;
+        const uint32_t in_tile = r - rpref[lo];
+        dst[u] = tpref[lo] + in_tile;
+        live[u] = r0 + u * kThreads < g_total && dst[u] < a.capacity;
+        src[u] = (t0 + lo) * kEscCap + in_tile;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -859,30 +890,47 @@ __global__ void __launch_bounds__(kThreads)
 
 // ------------------------------------------------------------------ K2c
 // Escape-heavy tiles (more escapes than a scratch slot holds): one CTA per
-// listed tile re-derives its escapes from the input in element order — 64
-// bytes of words per thread per round with all loads in flight, per-thread
-// escape masks from the marked LUT, one block scan for the ordinals.  The
-// grid is a fixed wave of CTAs striding over the list, so with no heavy tile
-// the launch costs one load per CTA.  (A single warp walking 32 words per
-// dependent load took ~0.5 ms per tile: 8.7 GB/s at 7.9% escapes.)
+// listed tile re-derives its escapes from the input in element order.  Per
+// round of 256 x 64 bytes: every thread loads its 64 bytes (all loads in
+// flight) and parks them in shared memory, builds its escape mask from the
+// marked LUT, one block scan gives each thread its first ordinal, threads
+// append the tile-local indices of their escapes to a compact shared list,
+// and then the whole CTA writes the round's records with consecutive threads
+// on consecutive ordinals (coalesced stores, work spread evenly however the
+// escapes cluster).  The grid is a fixed wave of CTAs striding over the list,
+// so with no heavy tile the launch costs one load per CTA.
+template <int FMT>
+constexpr int kHeavySmem = kThreads * 64 + kThreads * (64 / Fmt<FMT>::kWordBytes) * 2;
+
 template <int FMT, int POSB>
 __global__ void __launch_bounds__(kThreads)
     escape_heavy(const __grid_constant__ sz_params p, const GatherArgs a) {
   constexpr int WB = Fmt<FMT>::kWordBytes;
-  constexpr int EPT = 64 / WB;  // words per thread per round
-  __shared__ uint8_t lut[256];
+  constexpr int EPT = 64 / WB;              // words per thread per round
+  constexpr int RE = kThreads * EPT;        // elements per round
+  // escape-flag lane tables: tf[k][e] = escape(e) << k, so the sum of a
+  // 4-element group's lookups (lane k = element k) is its 4-bit flag nibble
+  // (t4_group's addressing, flags only); 64 B / 128 B / 1 KiB per lane
+  // for E4M3 / E5M2 / BF16
+  constexpr int TB = 1 << Fmt<FMT>::kExpBits;
+  __shared__ __align__(1024) uint32_t tf[4 * TB];
   __shared__ uint32_t hspine[kWarps];
+  extern __shared__ __align__(16) uint8_t heavy_smem[];     // kHeavySmem<FMT> bytes
+  uint32_t* const s_w = reinterpret_cast<uint32_t*>(heavy_smem);  // the round's words
+  uint16_t* const s_idx = reinterpret_cast<uint16_t*>(heavy_smem + kThreads * 64);  // escapes
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned int count = *a.heavy_count;
   if (blockIdx.x >= count) return;
-  for (int i = tid; i < 256; i += kThreads) lut[i] = p.enc_lut[i];
+  for (int i = tid; i < 4 * TB; i += kThreads)
+    tf[i] = static_cast<uint32_t>((p.enc_lut[i % TB] >> 4) & 1u) << (i / TB);
   __syncthreads();
+  const uint32_t tbase = smem_addr(tf);
   for (unsigned int li = blockIdx.x; li < count; li += gridDim.x) {
     const uint64_t tile = a.heavy_list[li];
     const uint64_t e_begin = tile * a.tile_elems;
     const uint64_t e_end = min(e_begin + a.tile_elems, a.n);
     uint64_t ord = a.heavy_pref[li];
-    for (uint64_t r0 = e_begin; r0 < e_end; r0 += static_cast<uint64_t>(kThreads) * EPT) {
+    for (uint64_t r0 = e_begin; r0 < e_end; r0 += RE) {
       const uint64_t my0 = r0 + static_cast<uint64_t>(tid) * EPT;
       uint32_t w[16];
 #pragma unroll
@@ -914,19 +962,40 @@ __global__ void __launch_bounds__(kThreads)
           }
         }
       }
+#pragma unroll
+      for (int q = 0; q < 16; q += 4)
+        *reinterpret_cast<uint4*>(&s_w[tid * 16 + q]) = make_uint4(w[q], w[q + 1], w[q + 2], w[q + 3]);
+      // elements of this thread inside the tile
+      const uint32_t nvalid =
+          e_end > my0 ? static_cast<uint32_t>(min(e_end - my0, static_cast<uint64_t>(EPT))) : 0u;
       uint32_t mask[EPT / 32];
       uint32_t cnt = 0;
 #pragma unroll
       for (int q = 0; q < EPT / 32; ++q) {
         uint32_t mk = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int el = q * 32 + j;
-          const uint32_t word = WB == 2 ? (w[el >> 1] >> (16 * (el & 1))) & 0xFFFFu
-                                        : (w[el >> 2] >> (8 * (el & 3))) & 0xFFu;
-          const bool in = my0 + el < e_end;
-          mk |= static_cast<uint32_t>(in && (lut[raw_exponent<FMT>(word)] & 0x10)) << j;
+        for (int g = 0; g < 8; ++g) {  // group of 4 elements -> flag nibble g
+          uint32_t t0, t1, t2, t3;
+          if constexpr (WB == 2) {
+            const uint32_t f0 = (w[2 * g] >> 5) & 0x03FC03FCu;  // 4e of elements 4g, 4g+1
+            const uint32_t f1 = (w[2 * g + 1] >> 5) & 0x03FC03FCu;
+            t0 = lds_u32_off<0>(tbase + (f0 & 0xFFFFu));
+            t1 = lds_u32_off<4 * TB>(tbase + (f0 >> 16));
+            t2 = lds_u32_off<8 * TB>(tbase + (f1 & 0xFFFFu));
+            t3 = lds_u32_off<12 * TB>(tbase + (f1 >> 16));
+          } else {
+            const uint32_t x = w[8 * q + g];
+            const uint32_t f = FMT == SZ_E5M2 ? (x & 0x7C7C7C7Cu)           // byte k = 4e
+                                              : ((x >> 1) & 0x3C3C3C3Cu);
+            t0 = lds_u32_off<0>(__byte_perm(f, tbase, 0x7650));
+            t1 = lds_u32_off<4 * TB>(__byte_perm(f, tbase, 0x7651));
+            t2 = lds_u32_off<8 * TB>(__byte_perm(f, tbase, 0x7652));
+            t3 = lds_u32_off<12 * TB>(__byte_perm(f, tbase, 0x7653));
+          }
+          mk |= (t0 + t1 + t2 + t3) << (4 * g);
         }
+        const uint32_t nv = nvalid > 32u * q ? nvalid - 32u * q : 0u;
+        if (nv < 32) mk &= (1u << nv) - 1u;
         mask[q] = mk;
         cnt += __popc(mk);
       }
@@ -946,25 +1015,29 @@ __global__ void __launch_bounds__(kThreads)
         wbase += v < warp ? t : 0;
         total += t;
       }
-      uint64_t o = ord + wbase + incl - cnt;
+      uint32_t r = wbase + incl - cnt;  // this thread's first round-relative ordinal
 #pragma unroll
       for (int q = 0; q < EPT / 32; ++q) {
         uint32_t mk = mask[q];
         while (mk) {
           const int j = __ffs(mk) - 1;
           mk &= mk - 1;
-          const int el = q * 32 + j;
-          const uint32_t word = WB == 2 ? (pick<16>(w, el >> 1) >> (16 * (el & 1))) & 0xFFFFu
-                                        : (pick<16>(w, el >> 2) >> (8 * (el & 3))) & 0xFFu;
-          if (o < a.capacity) {
-            a.values[o] = static_cast<uint8_t>(raw_exponent<FMT>(word));
-            put_position<POSB>(a.positions, o, my0 + el, a.chunk, a.chunk_shift);
-          }
-          ++o;
+          s_idx[r++] = static_cast<uint16_t>(tid * EPT + q * 32 + j);
+        }
+      }
+      __syncthreads();
+      const uint8_t* wb = reinterpret_cast<const uint8_t*>(s_w);
+      for (uint32_t k = tid; k < total; k += kThreads) {
+        const uint64_t o = ord + k;
+        if (o < a.capacity) {
+          const uint32_t el = s_idx[k];
+          const uint32_t word = WB == 2 ? reinterpret_cast<const uint16_t*>(wb)[el] : wb[el];
+          a.values[o] = static_cast<uint8_t>(raw_exponent<FMT>(word));
+          put_position<POSB>(a.positions, o, r0 + el, a.chunk, a.chunk_shift);
         }
       }
       ord += total;
-      __syncthreads();  // hspine reuse
+      __syncthreads();  // s_w / s_idx / hspine reuse
     }
   }
 }
@@ -1076,10 +1149,21 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
   escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups * g.split), kThreads, 0, s>>>(p, g);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const uint64_t heavy_grid = want * 8;  // one wave of 256-thread CTAs
+  // one wave of K2c CTAs (as many as fit per SM next to nothing else)
+  static const int heavy_per_sm = [] {
+    int blocks = 0;
+    if (cudaFuncSetAttribute(escape_heavy<FMT, POSB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kHeavySmem<FMT>) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, escape_heavy<FMT, POSB>, kThreads,
+                                                      kHeavySmem<FMT>) != cudaSuccess)
+      return 0;
+    return blocks;
+  }();
+  if (heavy_per_sm <= 0) return cudaErrorInvalidConfiguration;
+  const uint64_t heavy_grid = want * static_cast<uint64_t>(heavy_per_sm);
   escape_heavy<FMT, POSB><<<static_cast<unsigned>(heavy_grid < a.num_tiles ? heavy_grid
                                                                              : a.num_tiles),
-                             kThreads, 0, s>>>(p, g);
+                             kThreads, kHeavySmem<FMT>, s>>>(p, g);
   return cudaGetLastError();
 }
 

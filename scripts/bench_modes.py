@@ -9,6 +9,7 @@ whatever the profile puts outside them).  Device time: CUDA events, 3 warm-up
 + 5 timed round trips, bitwise verified first.  One JSON line per config.
 """
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -18,7 +19,8 @@ import torch  # noqa: E402
 import paper_2605_01708_b200 as sz  # noqa: E402
 from paper_2605_01708_b200.engine import DeviceCodec, synth_kv  # noqa: E402
 
-N = 1 << 31
+N = int(os.environ.get("SZ_MODES_N", 1 << 31))
+ONLY = sys.argv[1:]  # optional config names to run
 PAPER_H200 = {  # PAPER.md rows (H200) for the same modes, encode/decode GB/s
     "bf16 top16 explicit c1024": (613.3, 2181.8),
     "bf16 top8 3-bit c1024": (440.1, 710.5),
@@ -40,6 +42,8 @@ def profile(fmt):
 
 
 def run(name, fmt, words, k, bits, mode, chunk, pos):
+    if ONLY and name not in ONLY:
+        return
     bw, _ = profile(fmt)
     entries = tuple(e for e, _ in bw)[:k]
     book = sz.ExponentCodebook(fmt, entries, bits, mode)

@@ -12,14 +12,18 @@ from paper_2605_01708_b200.engine import DeviceCodec, synth_kv  # noqa: E402
 fmt_name = sys.argv[1] if len(sys.argv) > 1 else "bf16"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1 << 28
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+bits = int(sys.argv[4]) if len(sys.argv) > 4 else 4      # 3: top-8 book
+chunk = int(sys.argv[5]) if len(sys.argv) > 5 else 1024
 fmt = sz.ElementFormat.from_name(fmt_name)
 if fmt is sz.ElementFormat.BF16:
     bw, esc = tuple((0x70 + i, 0.72 ** i) for i in range(16)), tuple(range(0x10, 0x18))
 else:
     bw, esc = tuple((8 + i, 0.72 ** i) for i in range(16)), (0, 1, 2, 3, 28, 29, 30, 31)
 words = synth_kv(n, fmt, 7, bw, esc, 0.0016)
-book = sz.ExponentCodebook(fmt, tuple(e for e, _ in bw), 4, sz.CodebookMode.TOPK_EXPLICIT)
-cfg = sz.CodecConfig(fmt, codebook=book)
+book = sz.ExponentCodebook(fmt, tuple(e for e, _ in bw)[:1 << bits], bits,
+                          sz.CodebookMode.TOPK_EXPLICIT)
+cfg = sz.CodecConfig(fmt, bits, sz.CodebookMode.TOPK_EXPLICIT, chunk,
+                     sz.PositionMode.CHUNK_RELATIVE, book)
 eng = DeviceCodec(cfg, book, n)
 eng.ensure_capacity(words)
 for _ in range(reps):
