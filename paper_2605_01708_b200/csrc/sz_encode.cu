@@ -166,8 +166,12 @@ constexpr bool kE5FullByte = true;
 #else
 constexpr bool kE5FullByte = false;
 #endif
-template <int FMT> constexpr int kT4Entries = (FMT == SZ_BF16 || kE5FullByte) ? 256 : 32;
-template <int FMT, int CB> constexpr bool kUseT4 = CB == 4 && FMT != SZ_E4M3;
+template <int FMT>
+constexpr int kT4Entries = (FMT == SZ_BF16 || (FMT == SZ_E5M2 && kE5FullByte)) ? 256
+                           : (FMT == SZ_E5M2 ? 32 : 16);
+// Lane tables for every code width: with 3-bit codes the four lookups of a
+// group sum to its 12-bit code group (bits 0-11), flags still in bits 16-19.
+template <int FMT, int CB> constexpr bool kUseT4 = CB == 4 || CB == 3;
 
 template <int OFF>
 __device__ __forceinline__ uint32_t lds_u32_off(uint32_t saddr) {
@@ -209,6 +213,13 @@ __device__ __forceinline__ uint32_t t4_group(const uint32_t (&x)[8], int g, uint
     const uint32_t t1 = lds_u32_off<128>(__byte_perm(f, base, 0x7651));
     const uint32_t t2 = lds_u32_off<256>(__byte_perm(f, base, 0x7652));
     const uint32_t t3 = lds_u32_off<384>(__byte_perm(f, base, 0x7653));
+    return sum4(t0, t1, t2, t3, one);
+  } else if constexpr (FMT == SZ_E4M3) {
+    const uint32_t f = (x[g] >> 1) & 0x3C3C3C3Cu;  // byte k = 4 * exponent (4 bits)
+    const uint32_t t0 = lds_u32_off<0>(__byte_perm(f, base, 0x7650));
+    const uint32_t t1 = lds_u32_off<64>(__byte_perm(f, base, 0x7651));
+    const uint32_t t2 = lds_u32_off<128>(__byte_perm(f, base, 0x7652));
+    const uint32_t t3 = lds_u32_off<192>(__byte_perm(f, base, 0x7653));
     return sum4(t0, t1, t2, t3, one);
   } else {
     const uint32_t f0 = (x[2 * g] >> 5) & 0x03FC03FCu;      // 4e of elements 4g, 4g+1
@@ -273,7 +284,7 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
       if (TAIL && nv < EPV) {  // tail slot: no codes or flags beyond N (x is 0 there)
         const int v = min(max(nv - 4 * g, 0), 4);
         r[g] &= v >= 4 ? 0xFFFFFFFFu
-                       : (((1u << (4 * v)) - 1u) | (((1u << v) - 1u) << 16) |
+                       : (((1u << (CB * v)) - 1u) | (((1u << v) - 1u) << 16) |
                           (((1u << (3 * v)) - 1u) << 20));
       }
       any |= r[g];
@@ -284,9 +295,22 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
       for (int g = 0; g < G; ++g) fm |= ((r[g] >> 16) & 0xFu) << (4 * g);
     }
     uint32_t cw[CWORDS], sw[SWORDS];
+    if constexpr (CB == 4) {
 #pragma unroll
-    for (int i = 0; i < CWORDS; ++i) cw[i] = __byte_perm(r[2 * i], r[2 * i + 1], 0x5410);
-    if constexpr (FMT == SZ_BF16) {
+      for (int i = 0; i < CWORDS; ++i) cw[i] = __byte_perm(r[2 * i], r[2 * i + 1], 0x5410);
+    } else {
+      uint32_t grp[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) grp[g] = r[g] & 0xFFFu;
+      concat_groups<G, 12>(grp, cw);
+    }
+    if constexpr (FMT == SZ_E4M3) {
+      uint32_t grp[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        grp[g] = pack_nib4(((x[g] >> 4) & 0x08080808u) | (x[g] & 0x07070707u));
+      concat_groups<G, 16>(grp, sw);
+    } else if constexpr (FMT == SZ_BF16) {
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const uint32_t lo4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x6420);
@@ -426,10 +450,11 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       if constexpr (FMT == SZ_E5M2 && kE5FullByte) {  // e is the whole byte here
         const uint32_t m = p.enc_lut[(e >> 2) & 31];
         const uint32_t a = ((e >> 5) & 4u) | (e & 3u);
-        s_tab[i] = ((m & 0xFu) << (4 * k)) | (((m >> 4) & 1u) << (16 + k)) | (a << (20 + 3 * k));
+        s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k)) |
+                   (a << (20 + 3 * k));
       } else {
         const uint32_t m = p.enc_lut[e];
-        s_tab[i] = ((m & 0xFu) << (4 * k)) | (((m >> 4) & 1u) << (16 + k));
+        s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k));
       }
     }
   } else {
