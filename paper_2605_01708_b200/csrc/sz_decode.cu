@@ -664,14 +664,21 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           }
           const uint32_t nch = static_cast<uint32_t>(nk - 1), no = static_cast<uint32_t>(n_o);
           uint32_t cur = 0;  // srel[cur] <= the round's first ordinal
-          for (uint32_t b0 = 0; b0 < no; b0 += 32 * U) {
-            uint32_t pvs[U], vs[U];
+          // batch b + 1's loads are issued before batch b is processed: one
+          // exposed memory latency per tile, not one per 4 x 32 ordinals
+          uint32_t pvs[U], vs[U];
+          auto load_batch = [&](uint32_t b0, uint32_t (&pp)[U], uint32_t (&vv)[U]) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const uint32_t orl = b0 + 32 * u + lane;
-              pvs[u] = orl < no ? static_cast<uint32_t>(load_pos<POSB>(a.positions, o_lo + orl)) : 0u;
-              vs[u] = orl < no ? a.values[o_lo + orl] : 0u;
+              pp[u] = orl < no ? static_cast<uint32_t>(load_pos<POSB>(a.positions, o_lo + orl)) : 0u;
+              vv[u] = orl < no ? a.values[o_lo + orl] : 0u;
             }
+          };
+          load_batch(0, pvs, vs);
+          for (uint32_t b0 = 0; b0 < no; b0 += 32 * U) {
+            uint32_t npvs[U], nvs[U];
+            if (b0 + 32 * U < no) load_batch(b0 + 32 * U, npvs, nvs);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const uint32_t br = b0 + 32 * u;
@@ -715,6 +722,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
               }
               const uint64_t o = o_lo + orl;
               if (hit && o >= o_first) stage(idx, o - o_first, v);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              pvs[u] = npvs[u];
+              vs[u] = nvs[u];
             }
           }
         } else {

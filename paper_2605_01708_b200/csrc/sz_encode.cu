@@ -616,17 +616,17 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         S.fmask[q][fsw(slot)] = fm;
         if (fm) {  // rare: append (element, raw exponent) records for the writer
           uint32_t r = atomicAdd(&S.esc_n[q], static_cast<uint32_t>(__popc(fm)));
-          uint32_t f = fm;
+          // a tile past kEscCap records is re-derived whole by K2c: no record
+          // of it is used, so stop writing them
+          uint32_t f = r + __popc(fm) <= kEscCap ? fm : 0u;
           while (f) {  // compact loop; x[] read through selects (no local memory)
             const int j = __ffs(f) - 1;
             f &= f - 1;
             uint32_t word;
             if constexpr (WB == 2) word = (pick<8>(x[i], j >> 1) >> (16 * (j & 1))) & 0xFFFFu;
             else word = (pick<8>(x[i], j >> 2) >> (8 * (j & 3))) & 0xFFu;
-            if (r < kEscCap)
-              S.esc_rec[q][r] = static_cast<uint32_t>(slot * EPV + j) |
+            S.esc_rec[q][r++] = static_cast<uint32_t>(slot * EPV + j) |
                                 (raw_exponent<FMT>(word) << 16);
-            ++r;
           }
         }
       }
@@ -987,9 +987,13 @@ __global__ void __launch_bounds__(kThreads)
           }
         }
       }
+      // 16-byte chunk c of thread t at chunk c ^ ((t >> 1) & 3): each 8-lane
+      // store phase then covers all 32 banks (linear: 4-way conflicts)
+      const uint32_t csw = (tid >> 1) & 3;
 #pragma unroll
-      for (int q = 0; q < 16; q += 4)
-        *reinterpret_cast<uint4*>(&s_w[tid * 16 + q]) = make_uint4(w[q], w[q + 1], w[q + 2], w[q + 3]);
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(&s_w[tid * 16 + 4 * (q ^ csw)]) =
+            make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
       // elements of this thread inside the tile
       const uint32_t nvalid =
           e_end > my0 ? static_cast<uint32_t>(min(e_end - my0, static_cast<uint64_t>(EPT))) : 0u;
@@ -1056,7 +1060,9 @@ __global__ void __launch_bounds__(kThreads)
         const uint64_t o = ord + k;
         if (o < a.capacity) {
           const uint32_t el = s_idx[k];
-          const uint32_t word = WB == 2 ? reinterpret_cast<const uint16_t*>(wb)[el] : wb[el];
+          const uint32_t b = el * WB;  // byte of the round: thread b >> 6, chunk (b >> 4) & 3
+          const uint32_t phys = (b & ~0x30u) | ((((b >> 4) ^ (b >> 7)) & 3u) << 4);
+          const uint32_t word = WB == 2 ? *reinterpret_cast<const uint16_t*>(wb + phys) : wb[phys];
           a.values[o] = static_cast<uint8_t>(raw_exponent<FMT>(word));
           put_position<POSB>(a.positions, o, r0 + el, a.chunk, a.chunk_shift);
         }
