@@ -950,43 +950,64 @@ __global__ void __launch_bounds__(kThreads)
     tf[i] = static_cast<uint32_t>((p.enc_lut[i % TB] >> 4) & 1u) << (i / TB);
   __syncthreads();
   const uint32_t tbase = smem_addr(tf);
-  for (unsigned int li = blockIdx.x; li < count; li += gridDim.x) {
-    const uint64_t tile = a.heavy_list[li];
-    const uint64_t e_begin = tile * a.tile_elems;
-    const uint64_t e_end = min(e_begin + a.tile_elems, a.n);
-    uint64_t ord = a.heavy_pref[li];
-    for (uint64_t r0 = e_begin; r0 < e_end; r0 += RE) {
-      const uint64_t my0 = r0 + static_cast<uint64_t>(tid) * EPT;
-      uint32_t w[16];
+  // this thread's 64 bytes of round r0 (clipped at the tile end e_end)
+  auto load_round = [&](uint64_t r0, uint64_t e_end, uint32_t (&w)[16]) {
+    const uint64_t my0 = r0 + static_cast<uint64_t>(tid) * EPT;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // two 32-byte halves (a segment holds >= 32 B)
-        const uint64_t e = my0 + h * (32 / WB);
-        const uint64_t off = e * WB;
-        const uint8_t* src = a.words + off;
-        if (a.seg_addrs)
-          src = reinterpret_cast<const uint8_t*>(__ldg(a.seg_addrs + (off >> a.seg_shift))) +
-                (off & ((1ull << a.seg_shift) - 1));
-        if (e + 32 / WB <= e_end) {
-          const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src));
-          const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-          w[8 * h + 0] = v0.x; w[8 * h + 1] = v0.y; w[8 * h + 2] = v0.z; w[8 * h + 3] = v0.w;
-          w[8 * h + 4] = v1.x; w[8 * h + 5] = v1.y; w[8 * h + 6] = v1.z; w[8 * h + 7] = v1.w;
-        } else {
+    for (int h = 0; h < 2; ++h) {  // two 32-byte halves (a segment holds >= 32 B)
+      const uint64_t e = my0 + h * (32 / WB);
+      const uint64_t off = e * WB;
+      const uint8_t* src = a.words + off;
+      if (a.seg_addrs)
+        src = reinterpret_cast<const uint8_t*>(__ldg(a.seg_addrs + (off >> a.seg_shift))) +
+              (off & ((1ull << a.seg_shift) - 1));
+      if (e + 32 / WB <= e_end) {
+        const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src));
+        const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+        w[8 * h + 0] = v0.x; w[8 * h + 1] = v0.y; w[8 * h + 2] = v0.z; w[8 * h + 3] = v0.w;
+        w[8 * h + 4] = v1.x; w[8 * h + 5] = v1.y; w[8 * h + 6] = v1.z; w[8 * h + 7] = v1.w;
+      } else {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {  // clipped: whole words while inside
-            uint32_t v = 0;
+        for (int q = 0; q < 8; ++q) {  // clipped: whole words while inside
+          uint32_t v = 0;
 #pragma unroll
-            for (int b = 0; b < 4 / WB; ++b) {
-              const uint64_t j = q * (4 / WB) + b;
-              if (e + j < e_end) {
-                const uint32_t x = WB == 2 ? reinterpret_cast<const uint16_t*>(src)[j] : src[j];
-                v |= x << (8 * WB * b);
-              }
+          for (int b = 0; b < 4 / WB; ++b) {
+            const uint64_t j = q * (4 / WB) + b;
+            if (e + j < e_end) {
+              const uint32_t x = WB == 2 ? reinterpret_cast<const uint16_t*>(src)[j] : src[j];
+              v |= x << (8 * WB * b);
             }
-            w[8 * h + q] = v;
           }
+          w[8 * h + q] = v;
         }
       }
+    }
+  };
+  // Flat loop over (listed tile, round) with the next round's loads in
+  // flight while this one is classified and written.
+  unsigned int li = blockIdx.x;
+  uint64_t e_begin = static_cast<uint64_t>(a.heavy_list[li]) * a.tile_elems;
+  uint64_t e_end = min(e_begin + a.tile_elems, a.n);
+  uint64_t ord = a.heavy_pref[li];
+  uint64_t r0 = e_begin;
+  uint32_t w[16];
+  load_round(r0, e_end, w);
+  while (true) {
+    // the round after this one
+    unsigned int nli = li;
+    uint64_t nr0 = r0 + RE, ne_end = e_end, nbegin = e_begin;
+    if (nr0 >= e_end) {
+      nli = li + gridDim.x;
+      if (nli < count) {
+        nbegin = static_cast<uint64_t>(a.heavy_list[nli]) * a.tile_elems;
+        ne_end = min(nbegin + a.tile_elems, a.n);
+        nr0 = nbegin;
+      }
+    }
+    uint32_t wn[16];
+    if (nli < count) load_round(nr0, ne_end, wn);
+    {
+      const uint64_t my0 = r0 + static_cast<uint64_t>(tid) * EPT;
       // 16-byte chunk c of thread t at chunk c ^ ((t >> 1) & 3): each 8-lane
       // store phase then covers all 32 banks (linear: 4-way conflicts)
       const uint32_t csw = (tid >> 1) & 3;
@@ -1055,14 +1076,16 @@ __global__ void __launch_bounds__(kThreads)
         }
       }
       __syncthreads();
-      const uint8_t* wb = reinterpret_cast<const uint8_t*>(s_w);
+      // (explicit shared-space loads: the extern-smem pointers reach here as
+      // generic addresses)
+      const uint32_t w_sa = smem_addr(s_w), i_sa = smem_addr(s_idx);
       for (uint32_t k = tid; k < total; k += kThreads) {
         const uint64_t o = ord + k;
         if (o < a.capacity) {
-          const uint32_t el = s_idx[k];
+          const uint32_t el = lds_u16(i_sa + 2 * k);
           const uint32_t b = el * WB;  // byte of the round: thread b >> 6, chunk (b >> 4) & 3
           const uint32_t phys = (b & ~0x30u) | ((((b >> 4) ^ (b >> 7)) & 3u) << 4);
-          const uint32_t word = WB == 2 ? *reinterpret_cast<const uint16_t*>(wb + phys) : wb[phys];
+          const uint32_t word = WB == 2 ? lds_u16(w_sa + phys) : lds_u8(w_sa + phys);
           a.values[o] = static_cast<uint8_t>(raw_exponent<FMT>(word));
           put_position<POSB>(a.positions, o, r0 + el, a.chunk, a.chunk_shift);
         }
@@ -1070,6 +1093,14 @@ __global__ void __launch_bounds__(kThreads)
       ord += total;
       __syncthreads();  // s_w / s_idx / hspine reuse
     }
+    if (nli >= count) break;
+    if (nli != li) ord = a.heavy_pref[nli];
+    li = nli;
+    r0 = nr0;
+    e_end = ne_end;
+    e_begin = nbegin;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = wn[i];
   }
 }
 
