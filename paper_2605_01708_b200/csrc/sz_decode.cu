@@ -112,6 +112,10 @@ __global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) 
   }
 }
 
+// decode tile: kDecItems 32-byte slots per decode thread
+constexpr int kDecItems = 2;
+constexpr int kDecSlots = kDecItems * kThreads;        // 512 slots per tile
+
 // ------------------------------------------------------------------ K3s
 // Sentinel mode (codec.py:459-467): escapes are marked in-band by the top
 // code, so an escape's ordinal is the number of marks before it.  This pass
@@ -175,8 +179,31 @@ __global__ void __launch_bounds__(kThreads)
   const int lane = threadIdx.x & 31;
   const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  // 4-bit codes, whole tile inside the stream: the tile's code plane as
+  // 16-byte loads, all in flight at once; a mark is a nibble of all ones, so
+  // the count is popc of the nibble-AND (no per-slot mask gather)
+  constexpr int kVec = CB == 4 ? kDecSlots * CBYTES / 16 / 32 : 0;  // uint4 per lane
   for (uint64_t t = gw; t < num_tiles; t += nw) {   // one warp per tile
     uint32_t cnt = 0;
+    if constexpr (CB == 4) {
+      if ((t + 1) * tile_slots * EPV <= n && !(reinterpret_cast<uintptr_t>(codes) & 15)) {
+        const uint4* q = reinterpret_cast<const uint4*>(codes + t * tile_slots * CBYTES);
+        uint4 v[kVec];
+#pragma unroll
+        for (int i = 0; i < kVec; ++i) v[i] = __ldg(q + lane + 32 * i);
+#pragma unroll
+        for (int i = 0; i < kVec; ++i) {
+          const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            cnt += __popc(w4[k] & (w4[k] >> 1) & (w4[k] >> 2) & (w4[k] >> 3) & 0x11111111u);
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        if (lane == 0) tile_marks[t] = cnt;
+        continue;
+      }
+    }
     for (uint32_t j = lane; j < tile_slots; j += 32) {
       const uint64_t e0 = (t * tile_slots + j) * EPV;
       if (e0 >= n) break;
@@ -194,6 +221,31 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
     if (lane == 0) tile_marks[t] = cnt;
+  }
+}
+
+// ------------------------------------------------------------------ K3a
+// abs32 mode: first escape ordinal of every decode tile.  Positions are
+// ascending element indices (codec.py:500-507), so ordinal o opens tiles
+// (tile(pos[o-1]), tile(pos[o])]; one coalesced pass over the positions
+// writes every boundary once (a per-tile binary search would be ~20
+// dependent memory latencies).  Unsorted (corrupt) streams leave some
+// boundaries at their zeroed value; the decoder clamps, and flags them.
+__global__ void __launch_bounds__(kThreads)
+    abs_bounds_kernel(const uint32_t* __restrict__ pos, const uint64_t* m_ptr, uint64_t m_host,
+                      uint64_t n, uint64_t tile_elems, uint64_t num_tiles,
+                      uint64_t* __restrict__ bounds) {
+  const uint64_t m = m_ptr ? min(*m_ptr, n) : m_host;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t first = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  auto tile_of = [&](uint64_t o) -> uint64_t {  // tile holding ordinal o's element
+    const uint64_t t = pos[o] / tile_elems;
+    return t < num_tiles ? t : num_tiles;
+  };
+  for (uint64_t o = first; o <= m; o += stride) {
+    const uint64_t t_prev = o == 0 ? 0 : tile_of(o - 1) + 1;  // first tile not before o-1
+    const uint64_t t_cur = o == m ? num_tiles : tile_of(o);
+    for (uint64_t b = t_prev; b <= t_cur; ++b) bounds[b] = o;
   }
 }
 
@@ -300,26 +352,6 @@ __device__ __forceinline__ uint32_t escape_value(const uint8_t* vals, uint32_t f
   return ofirst + c < m ? gvals[ofirst + c] : 0u;
 }
 
-// Warp-cooperative lower_bound over sorted u32 positions [0, m) (abs32 mode).
-__device__ uint64_t warp_lower_bound(const uint32_t* pos, uint64_t m, uint64_t target) {
-  const int lane = threadIdx.x & 31;
-  uint64_t lo = 0, hi = m;  // answer in [lo, hi]
-  while (hi - lo > 32) {
-    const uint64_t step = (hi - lo) / 33 + 1;
-    const uint64_t probe = lo + (lane + 1) * step;
-    const bool less = probe < hi && pos[probe - 1] < target;  // all < probe are < target
-    const uint32_t bal = __ballot_sync(0xffffffffu, less);
-    const int cnt = __popc(bal);  // lanes 0..cnt-1 say "less" (monotone if sorted)
-    const uint64_t nlo = lo + cnt * step;
-    const uint64_t nhi = min(hi, lo + (cnt + 1) * step);
-    lo = nlo;
-    hi = max(nhi, nlo);
-  }
-  const uint64_t probe = lo + lane;
-  const bool less = probe < hi && pos[probe] < target;
-  return lo + __popc(__ballot_sync(0xffffffffu, less));
-}
-
 // ------------------------------------------------------------------ K4 (persistent)
 // Explicit modes (chunk-relative and abs32).  Same warp-specialised shape as
 // the encoder: warp 8 streams each tile's code and sign|mantissa planes into a
@@ -327,8 +359,6 @@ __device__ uint64_t warp_lower_bound(const uint32_t* pos, uint64_t m, uint64_t t
 // (bitmap + raw values in smem) and runs every per-escape check; warps 0-7
 // decode slots from smem and write 256-bit stores.  No CTA-wide barriers in
 // steady state — only mbarrier hand-offs.
-constexpr int kDecItems = 2;
-constexpr int kDecSlots = kDecItems * kThreads;        // 512 slots per tile
 constexpr int kDecHelpers = 3;                          // escape-staging warps
 constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
 constexpr int kDecOffStage = 256;                       // staged chunk offsets per helper
@@ -579,9 +609,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           }
         }
       } else if constexpr (ABS) {
+        // the tile's ordinal range from K3a (abs_bounds_kernel); clamped,
+        // so a corrupt (unsorted) stream only ever costs bounded reads
         const uint32_t* pos = static_cast<const uint32_t*>(a.positions);
-        const uint64_t lo = warp_lower_bound(pos, m, s0);
-        const uint64_t hi = max(lo, warp_lower_bound(pos, m, s1));
+        const uint64_t lo = min(a.offsets[tile], m);
+        const uint64_t hi = max(lo, min(a.offsets[tile + 1], m));
         o_first = lo;
         for (uint64_t o = lo + lane; o < hi; o += 32) {
           const uint64_t idx = pos[o];
@@ -965,8 +997,10 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   const bool chunked = !p->sentinel && !p->abs32;
   const uint64_t dtiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
   // scanned counts: per-chunk escape counts, or (sentinel) per-tile marks
+  // abs32: the scanned array is replaced by per-tile ordinal bounds (K3a)
   const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size
                                    : (p->sentinel ? dtiles : 0);
+  const uint64_t nbounds = p->abs32 ? dtiles + 1 : 0;
   const uint64_t otiles = nchunks ? offsets_tiles(nchunks) : 0;
   uint64_t* b = static_cast<uint64_t*>(base);
   // zeroed region first: look-back states + counters
@@ -974,9 +1008,9 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   w.off_counter = reinterpret_cast<unsigned long long*>(b + otiles);
   w.dec_states = b + otiles + 1;
   w.dec_counter = reinterpret_cast<unsigned long long*>(b + otiles + 1 + dtiles);
-  w.zero_bytes = (otiles + dtiles + 2) * sizeof(uint64_t);
-  w.offsets = b + otiles + dtiles + 2;
-  w.tile_marks = reinterpret_cast<uint32_t*>(w.offsets + (nchunks ? nchunks + 1 : 0));
+  w.zero_bytes = (otiles + dtiles + 2 + nbounds) * sizeof(uint64_t);
+  w.offsets = b + otiles + dtiles + 2;  // (abs32 bounds: inside the zeroed prefix)
+  w.tile_marks = reinterpret_cast<uint32_t*>(w.offsets + (nchunks ? nchunks + 1 : nbounds));
   w.total = w.zero_bytes + (nchunks ? (nchunks + 1) * sizeof(uint64_t) : 0) +
             (p->sentinel ? dtiles * sizeof(uint32_t) : 0) + 256;
   return w;
@@ -1077,6 +1111,14 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
       case 4: marks_kernel<SZ_E4M3, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
       default: marks_kernel<SZ_E4M3, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
     }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return sz_record_cuda(e);
+  }
+  if (p->abs32) {
+    const unsigned g = static_cast<unsigned>(sm_count() * 8);
+    abs_bounds_kernel<<<g, kThreads, 0, s>>>(static_cast<const uint32_t*>(in->d_positions),
+                                             in->d_n_escapes, m, n, decode_tile_for(p->fmt),
+                                             dtiles, w.offsets);
     e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
