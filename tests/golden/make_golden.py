@@ -223,6 +223,97 @@ def main():
     mutate("m_mismatch", escape_values=vals[:-1])
     mutate("clean")
 
+    # 7b. Corruption verdicts of the other modes: abs32 positions, sentinel
+    #     marks, E5M2 values (5-bit domain), 3-bit codes past a short book.
+    bases = {}
+
+    def make_base(bid, fmt, words, code_bits, mode, chunk, pos, book):
+        stream = sz.RawTensorStream(fmt, np.asarray(words, dtype=fmt.word_dtype))
+        cb = sz.ExponentCodebook(fmt, tuple(book), code_bits, mode)
+        bcfg = sz.CodecConfig(fmt, code_bits, mode, chunk, pos, cb)
+        benc = sz.encode(stream, bcfg)
+        arrays[f"corrupt_base_{bid}/words"] = stream.words
+        bases[bid] = {"fmt": FMT_ID[fmt], "code_bits": code_bits, "sentinel": mode is SENT,
+                      "chunk": chunk, "abs32": pos is ABS, "book": [int(e) for e in book]}
+
+        def bmutate(cid, **fields):
+            kw = dict(n_elements=benc.n_elements, n_escapes=benc.n_escapes,
+                      packed_codes=benc.packed_codes, sign_mantissa=benc.sign_mantissa,
+                      chunk_counts=benc.chunk_counts, escape_positions=benc.escape_positions,
+                      escape_values=benc.escape_values, codebook=benc.codebook)
+            kw.update(fields)
+            try:
+                sz.decode(EncodedStreams(**kw), bcfg, benc.codebook)
+                verdict = {"raised": None, "chunk": None}
+            except sz.SplitZipError as exc:
+                verdict = {"raised": type(exc).__name__, "chunk": getattr(exc, "chunk", None)}
+            q = f"corrupt_{cid}/"
+            arrays[q + "packed_codes"] = np.frombuffer(kw["packed_codes"], np.uint8)
+            arrays[q + "sign_mantissa"] = np.frombuffer(kw["sign_mantissa"], np.uint8)
+            arrays[q + "chunk_counts"] = np.asarray(kw["chunk_counts"], np.uint32)
+            arrays[q + "escape_positions"] = np.asarray(kw["escape_positions"])
+            arrays[q + "escape_values"] = np.asarray(kw["escape_values"], np.uint8)
+            corrupt.append({"id": cid, "base": bid, "n": kw["n_elements"],
+                            "m": kw["n_escapes"], **verdict})
+        return benc, bmutate
+
+    def set_code(packed, i, code, bits):
+        buf = bytearray(packed)
+        for b in range(bits):
+            bit = i * bits + b
+            if (code >> b) & 1:
+                buf[bit >> 3] |= 1 << (bit & 7)
+            else:
+                buf[bit >> 3] &= ~(1 << (bit & 7)) & 0xFF
+        return bytes(buf)
+
+    b16 = tuple(e for e, _ in B16)
+    # abs32 positions (codec.py:500-507)
+    benc, bm = make_base("abs", BF16, exact(BF16, 3000, 0.01, 21, B16, EB), 4, EXPL, 1024,
+                         ABS, b16)
+    pos = benc.escape_positions.copy()
+    pos[3], pos[4] = pos[4], pos[3]
+    bm("abs_not_increasing", escape_positions=pos)
+    pos = benc.escape_positions.copy()
+    pos[-1] = benc.n_elements
+    bm("abs_past_end", escape_positions=pos)
+    vals = benc.escape_values.copy()
+    vals[2] = b16[0]
+    bm("abs_value_in_book", escape_values=vals)
+    bm("abs_m_mismatch", escape_values=benc.escape_values[:-1])
+    bm("abs_clean")
+    # sentinel marks (codec.py:459-467)
+    benc, bm = make_base("sent", BF16, exact(BF16, 3000, 0.01, 22, B16, EB), 4, SENT, 1024,
+                         CHUNK, b16[:15])
+    codes_u = np.frombuffer(benc.packed_codes, np.uint8)
+    nib = np.stack([codes_u & 15, codes_u >> 4], axis=1).reshape(-1)[:benc.n_elements]
+    plain = int(np.flatnonzero(nib != 15)[7])
+    mark = int(np.flatnonzero(nib == 15)[3])
+    bm("sent_extra_mark", packed_codes=set_code(benc.packed_codes, plain, 15, 4))
+    bm("sent_lost_mark", packed_codes=set_code(benc.packed_codes, mark, 0, 4))
+    vals = benc.escape_values.copy()
+    vals[1] = b16[0]
+    bm("sent_value_in_book", escape_values=vals)
+    bm("sent_clean")
+    # E5M2 escape values: 5-bit domain (codec.py:451-457)
+    benc, bm = make_base("e5", E5M2, exact(E5M2, 4000, 0.01, 23, E16, EE), 4, EXPL, 1024,
+                         CHUNK, tuple(e for e, _ in E16))
+    vals = benc.escape_values.copy()
+    vals[4] = 40
+    bm("e5_value_domain", escape_values=vals)
+    vals = benc.escape_values.copy()
+    vals[6] = 8
+    bm("e5_value_in_book", escape_values=vals)
+    pos = benc.escape_positions.copy()
+    pos[0] = 1500
+    bm("e5_pos_over_chunk", escape_positions=pos)
+    bm("e5_clean")
+    # 3-bit codes with a 6-entry book: codes 6 and 7 decode nothing
+    benc, bm = make_base("tri", BF16, exact(BF16, 3000, 0.01, 24, B16, EB), 3, EXPL, 1024,
+                         CHUNK, b16[:6])
+    bm("tri_code_range", packed_codes=set_code(benc.packed_codes, 1234, 7, 3))
+    bm("tri_clean")
+
     # 8. Container parse verdicts (container.py:225-296) on mutated bytes of a
     #    valid BF16 container and an E5M2 one (5-bit values section).
     cverdicts = []
@@ -260,7 +351,8 @@ def main():
     np.savez_compressed(HERE / "golden.npz", **arrays)
     (HERE / "manifest.json").write_text(json.dumps(
         {"generator": "tests/golden/make_golden.py (reference splitzip 0.1.0)",
-         "cases": cases, "corruptions": corrupt, "container_verdicts": cverdicts}, indent=1))
+         "cases": cases, "corruptions": corrupt, "corruption_bases": bases,
+         "container_verdicts": cverdicts}, indent=1))
     print(f"{len(cases)} cases, {len(corrupt)} corruption verdicts, "
           f"{(HERE / 'golden.npz').stat().st_size} bytes")
 

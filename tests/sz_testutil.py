@@ -24,6 +24,27 @@ class Golden:
         self._npz = np.load(GOLDEN_DIR / "golden.npz")
         self.cases = self.manifest["cases"]
         self.corruptions = self.manifest["corruptions"]
+        self.corruption_bases = self.manifest.get("corruption_bases", {})
+
+    def corruption_base(self, verdict: dict):
+        """(base descriptor, original words) of a corruption verdict; verdicts
+        without a base mutate the BF16 explicit chunk-relative encode whose
+        book is the top 16 of its own histogram."""
+        bid = verdict.get("base")
+        if bid is None:
+            return None, self.arr("corrupt", "words")
+        return self.corruption_bases[bid], self.arr(f"corrupt_base_{bid}", "words")
+
+    def corruption_sections(self, verdict: dict) -> dict:
+        pre = f"corrupt_{verdict['id']}"
+        return {
+            "n": verdict["n"], "m": verdict["m"],
+            "packed_codes": self.arr(pre, "packed_codes").tobytes(),
+            "sign_mantissa": self.arr(pre, "sign_mantissa").tobytes(),
+            "chunk_counts": self.arr(pre, "chunk_counts"),
+            "escape_positions": self.arr(pre, "escape_positions"),
+            "escape_values": self.arr(pre, "escape_values"),
+        }
 
     def arr(self, cid: str, name: str) -> np.ndarray:
         return self._npz[f"{cid}/{name}"]

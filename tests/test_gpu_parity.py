@@ -71,15 +71,23 @@ def test_histogram_matches_reference(cid):
 def test_corruption_verdicts_match_reference(verdict):
     m = sz()
     g = golden()
-    words = g.arr("corrupt", "words")
-    stream = m.RawTensorStream(m.ElementFormat.BF16, words)
-    book = m.select_codebook(m.build_histogram(stream), 4, m.CodebookMode.TOPK_EXPLICIT)
-    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
-    pre = f"corrupt_{verdict['id']}"
+    base, words = g.corruption_base(verdict)
+    if base is None:
+        fmt = m.ElementFormat.BF16
+        book = m.select_codebook(m.build_histogram(m.RawTensorStream(fmt, words)), 4,
+                                 m.CodebookMode.TOPK_EXPLICIT)
+        cfg = m.CodecConfig(fmt, codebook=book)
+    else:
+        fmt = list(m.ElementFormat)[base["fmt"]]
+        mode = m.CodebookMode.TOP15_SENTINEL if base["sentinel"] else m.CodebookMode.TOPK_EXPLICIT
+        book = m.ExponentCodebook(fmt, tuple(base["book"]), base["code_bits"], mode)
+        cfg = m.CodecConfig(fmt, base["code_bits"], mode, base["chunk"],
+                            m.PositionMode.ABSOLUTE_32 if base["abs32"]
+                            else m.PositionMode.CHUNK_RELATIVE, book)
+    sec = g.corruption_sections(verdict)
     streams = m.EncodedStreams(
-        verdict["n"], verdict["m"], g.arr(pre, "packed_codes").tobytes(),
-        g.arr(pre, "sign_mantissa").tobytes(), g.arr(pre, "chunk_counts"),
-        g.arr(pre, "escape_positions"), g.arr(pre, "escape_values"), book)
+        sec["n"], sec["m"], sec["packed_codes"], sec["sign_mantissa"], sec["chunk_counts"],
+        sec["escape_positions"], sec["escape_values"], book)
     if verdict["raised"] is None:
         assert np.array_equal(m.decode(streams, cfg, book).words, words)
         return
