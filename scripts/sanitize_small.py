@@ -11,14 +11,16 @@ from oracle import sz_oracle as O  # noqa: E402
 
 for fmt_id, fmt, bk, esc in ((0, sz.ElementFormat.BF16, O.BF16_BOOK, O.BF16_ESC),
                              (1, sz.ElementFormat.FP8_E5M2, O.E5M2_BOOK, O.E5M2_ESC)):
-    for rate, chunk, mode, pos in ((0.0016, 1024, "explicit", "chunk"), (0.3, 256, "explicit", "chunk"),
-                                   (0.01, 3000, "explicit", "chunk"), (0.01, 1024, "explicit", "abs32"),
-                                   (0.01, 1024, "sentinel", "chunk")):
+    for rate, chunk, mode, pos, bits in (
+            (0.0016, 1024, "explicit", "chunk", 4), (0.3, 256, "explicit", "chunk", 4),
+            (0.01, 3000, "explicit", "chunk", 4), (0.01, 1024, "explicit", "abs32", 4),
+            (0.01, 1024, "sentinel", "chunk", 4), (0.07, 1024, "explicit", "chunk", 3),
+            (0.3, 1024, "explicit", "abs32", 4)):
         n = 200_003
         words = O.exact_stream(fmt_id, n, rate, 5, bk, esc)
         m = sz.CodebookMode.from_name(mode)
-        book = tuple(e for e, _ in bk)[: (15 if mode == "sentinel" else 16)]
-        cfg = sz.CodecConfig(fmt, 4, m, chunk, pos, sz.ExponentCodebook(fmt, book, 4, m))
+        book = tuple(e for e, _ in bk)[: (15 if mode == "sentinel" else (1 << bits))]
+        cfg = sz.CodecConfig(fmt, bits, m, chunk, pos, sz.ExponentCodebook(fmt, book, bits, m))
         st = sz.RawTensorStream(fmt, torch.from_numpy(words).cuda())
         enc = sz.encode(st, cfg)
         dec = sz.decode(enc, cfg, enc.codebook)
