@@ -201,6 +201,16 @@ int sz_compare(const void* d_a, const void* d_b, uint64_t n, uint32_t word_bytes
 int sz_encode_segments(const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
                        const sz_params* p, const sz_encoded* out, void* d_ws,
                        size_t ws_bytes, void* stream);
+/* As sz_encode_segments, given a virtual-address window [va_lo, va_hi) that
+ * contains every segment (e.g. the span of the KV-cache tensors) and with
+ * every segment 128-byte aligned: full tiles then arrive through a 2-D
+ * tensor map over the window (128B-swizzled boxes of min(seg_bytes, 32 KiB)),
+ * as the contiguous encoder's do.  Needs seg_bytes >= 1 KiB and a window of
+ * < 256 GiB; otherwise (or with va_hi <= va_lo) it is sz_encode_segments.
+ * No segment is read outside itself; the window only names addresses. */
+int sz_encode_segments_va(const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
+                          uint64_t va_lo, uint64_t va_hi, const sz_params* p,
+                          const sz_encoded* out, void* d_ws, size_t ws_bytes, void* stream);
 int sz_decode_segments(const sz_encoded_in* in, const sz_params* p,
                        const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
                        sz_decode_status* d_status, void* d_ws, size_t ws_bytes,

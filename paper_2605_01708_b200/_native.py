@@ -80,6 +80,8 @@ _SIGNATURES = {
     "sz_synth_words": (C.c_int, [_P, _U64, _U32, _U64, _P, _P, _U32, _P]),
     "sz_encode_segments": (C.c_int, [_P, _U64, _U64, C.POINTER(SzParams), C.POINTER(SzEncoded),
                                      _P, C.c_size_t, _P]),
+    "sz_encode_segments_va": (C.c_int, [_P, _U64, _U64, _U64, _U64, C.POINTER(SzParams),
+                                        C.POINTER(SzEncoded), _P, C.c_size_t, _P]),
     "sz_decode_segments": (C.c_int, [C.POINTER(SzEncodedIn), C.POINTER(SzParams), _P, _U64, _U64,
                                      _P, _P, C.c_size_t, _P]),
     "sz_peer_signal": (C.c_int, [_P, _U64, _P]),

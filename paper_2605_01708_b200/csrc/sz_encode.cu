@@ -79,6 +79,12 @@ struct EncodeArgs {
   const uint64_t* seg_addrs;
   uint32_t seg_shift;
   uint32_t k_lo, k_hi;      // 1057 << 10, 1057 (e5m2_sm_hi)
+  // segmented input with a tensor map over the virtual-address window that
+  // holds every segment: full tiles arrive as 2-D boxes of min(segment,
+  // tile) bytes at row (addr - seg_va_lo) / 128, 128B-swizzled like the
+  // contiguous path (use_tmap is then set too)
+  uint64_t seg_va_lo;
+  int32_t seg_tmap;
 };
 
 struct EncSmem {
@@ -480,16 +486,31 @@ __global__ void __launch_bounds__(kEncThreads, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       long long t_in = 0, t_scan = 0;
+      // Paged input: the tile is claimed one iteration ahead and its first
+      // segment address loaded before the stage waits, so neither the
+      // claim's atomic nor the segment-table load sits between a free stage
+      // and its TMA.
+      const bool ahead = a.seg_addrs != nullptr;
+      uint64_t next = ahead ? atomicAdd(a.tile_counter, 1ull) : 0;
       for (uint32_t it = 0;; ++it) {
         const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
         const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
+        uint64_t seg_first = 0;
+        if (ahead && next < a.num_tiles)
+          seg_first = __ldg(a.seg_addrs + ((next * TILE * WB) >> a.seg_shift));
         const long long c0 = SZ_CLOCK();
         mbar_wait(&S.in_empty[s], sph ^ 1);
         const long long c1 = SZ_CLOCK();
         mbar_wait(&S.scan_empty[q], qph ^ 1);
         t_in += c1 - c0;
         t_scan += SZ_CLOCK() - c1;
-        const uint64_t tile = atomicAdd(a.tile_counter, 1ull);
+        uint64_t tile;
+        if (ahead) {
+          tile = next;
+          if (tile < a.num_tiles) next = atomicAdd(a.tile_counter, 1ull);
+        } else {
+          tile = atomicAdd(a.tile_counter, 1ull);
+        }
         if (tile >= a.num_tiles) {
           // end markers in this slot and the next kWriterWarps-1 (one per
           // writer residue class); the dense warps relay them (computed)
@@ -506,7 +527,21 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         const uint64_t e0 = tile * TILE;
         const uint32_t full_slots = static_cast<uint32_t>(min(n - e0, TILE) / EPV);
         const uint32_t bytes = full_slots * 32;
-        if (a.seg_addrs) {
+        if (a.seg_tmap && e0 + TILE <= n) {
+          // paged KV through the VA-window tensor map: one swizzled box per
+          // segment (or per tile, for segments >= a tile)
+          mbar_arrive_tx(&S.full[s], kEncTileBytes);
+          const uint64_t b0 = e0 * WB, seg_mask = (1ull << a.seg_shift) - 1;
+          const uint32_t piece = static_cast<uint32_t>(
+              min(static_cast<uint64_t>(kEncTileBytes), seg_mask + 1));
+          for (uint32_t o = 0; o < static_cast<uint32_t>(kEncTileBytes); o += piece) {
+            const uint64_t g = b0 + o;
+            const uint64_t addr =
+                (o == 0 ? seg_first : __ldg(a.seg_addrs + (g >> a.seg_shift))) + (g & seg_mask);
+            tma_load_2d(S.in[s] + o, &tmap, 0, static_cast<int32_t>((addr - a.seg_va_lo) >> 7),
+                        &S.full[s]);
+          }
+        } else if (a.seg_addrs) {
           // paged KV: one bulk copy per (tile ∩ segment) piece, straight from
           // the cache blocks — no gather pass through HBM
           if (bytes) mbar_arrive_tx(&S.full[s], bytes);
@@ -1252,7 +1287,8 @@ cudaError_t dispatch_cb(int posb, const sz_params& p, const EncodeArgs& a, const
 // boxes of 256 rows = one 32 KiB encoder tile, 128B swizzle.  Returns false
 // (caller falls back to 1-D bulk copies) when the driver entry point is
 // unavailable or the input has no full tile.
-bool make_input_tmap(const void* words, uint64_t n_bytes, CUtensorMap* tm) {
+bool make_input_tmap(const void* words, uint64_t n_bytes, CUtensorMap* tm,
+                     uint32_t box_rows = kEncTileBytes / 128) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode_fn = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -1261,10 +1297,10 @@ bool make_input_tmap(const void* words, uint64_t n_bytes, CUtensorMap* tm) {
       fn = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
-  if (!encode_fn || n_bytes < static_cast<uint64_t>(kEncTileBytes)) return false;
+  if (!encode_fn || n_bytes < static_cast<uint64_t>(box_rows) * 128) return false;
   const cuuint64_t dims[2] = {128, n_bytes / 128};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {128, kEncTileBytes / 128};
+  const cuuint32_t box[2] = {128, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return encode_fn(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(words), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1291,7 +1327,7 @@ namespace {
 // d_words null, segment table + log2 segment bytes).
 int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shift, uint64_t n,
                 const sz_params* p, const sz_encoded* out, void* d_ws, size_t ws_bytes,
-                void* stream) {
+                void* stream, uint64_t va_lo = 0, uint64_t va_hi = 0) {
   if (int rc = sz_check_params(p, 0)) return rc;
   if (n == 0 || !out || (!d_words && !seg_addrs)) return SZ_ECONFIG;
   if ((reinterpret_cast<uintptr_t>(d_words) & 31) ||
@@ -1384,7 +1420,20 @@ int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shi
     a.dbg = dbg;
   }
   alignas(64) CUtensorMap tm{};
-  a.use_tmap = !seg_addrs && make_input_tmap(d_words, n * (p->fmt == SZ_BF16 ? 2 : 1), &tm);
+  if (!seg_addrs) {
+    a.use_tmap = make_input_tmap(d_words, n * (p->fmt == SZ_BF16 ? 2 : 1), &tm);
+  } else if (va_hi > va_lo && !(va_lo & 127) && seg_shift >= 10 &&
+             (va_hi - va_lo) / 128 < (1ull << 31)) {
+    // segments of >= 1 KiB (whole 8-row swizzle atoms) inside a window whose
+    // rows fit the int32 box coordinate
+    const uint64_t seg = 1ull << seg_shift;
+    const uint32_t rows = static_cast<uint32_t>(
+        (seg < static_cast<uint64_t>(kEncTileBytes) ? seg : kEncTileBytes) / 128);
+    a.seg_tmap = make_input_tmap(reinterpret_cast<const void*>(va_lo),
+                                 (va_hi - va_lo + 127) & ~127ull, &tm, rows);
+    a.use_tmap = a.seg_tmap;
+    a.seg_va_lo = va_lo;
+  }
   const int posb = pos_bytes(p);
   switch (p->fmt) {
     case SZ_BF16: e = dispatch_cb<SZ_BF16>(posb, *p, a, g, tm, s); break;
@@ -1426,11 +1475,18 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p, const sz_enco
 int sz_encode_segments(const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
                        const sz_params* p, const sz_encoded* out, void* d_ws, size_t ws_bytes,
                        void* stream) {
+  return sz_encode_segments_va(d_seg_addrs, n_segs, seg_bytes, 0, 0, p, out, d_ws, ws_bytes,
+                               stream);
+}
+
+int sz_encode_segments_va(const uint64_t* d_seg_addrs, uint64_t n_segs, uint64_t seg_bytes,
+                          uint64_t va_lo, uint64_t va_hi, const sz_params* p,
+                          const sz_encoded* out, void* d_ws, size_t ws_bytes, void* stream) {
   if (!p || !d_seg_addrs || n_segs == 0 || seg_bytes < 32 || (seg_bytes & (seg_bytes - 1)))
     return SZ_ECONFIG;
   const uint64_t wb = p->fmt == SZ_BF16 ? 2 : 1;
   return encode_impl(nullptr, d_seg_addrs, static_cast<uint32_t>(__builtin_ctzll(seg_bytes)),
-                     n_segs * seg_bytes / wb, p, out, d_ws, ws_bytes, stream);
+                     n_segs * seg_bytes / wb, p, out, d_ws, ws_bytes, stream, va_lo, va_hi);
 }
 
 }  // extern "C"

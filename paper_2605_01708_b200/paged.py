@@ -32,7 +32,7 @@ from .codec import (CodecConfig, EncodeBuffers, EncodedStreams, _config_params,
 from .errors import ConfigError
 from .formats import packed_nbytes
 
-__all__ = ["kv_block_table", "encode_segments", "decode_segments", "encode_kv_blocks",
+__all__ = ["kv_block_table", "kv_va_window", "encode_segments", "decode_segments", "encode_kv_blocks",
            "decode_kv_blocks"]
 
 
@@ -75,10 +75,25 @@ def _need_book(config: CodecConfig) -> ExponentCodebook:
     return config.codebook
 
 
+def kv_va_window(kv_caches: Sequence[torch.Tensor] | torch.Tensor) -> tuple[int, int] | None:
+    """Virtual-address window [lo, hi) spanning the KV-cache tensors, or None
+    when a block could sit off the 128-byte grid (then the encoder keeps its
+    1-D bulk copies).  Host-side only: tensor base pointers and strides."""
+    caches = [kv_caches] if isinstance(kv_caches, torch.Tensor) else list(kv_caches)
+    if any(c.data_ptr() % 128 or (c.stride(0) * c.element_size()) % 128 for c in caches):
+        return None
+    lo = min(c.data_ptr() for c in caches)
+    hi = max(c.data_ptr() + c.numel() * c.element_size() for c in caches)
+    return lo, hi
+
+
 def encode_segments(seg_addrs: torch.Tensor, seg_bytes: int, config: CodecConfig, *,
-                    capacity: int | None = None) -> EncodedStreams:
+                    capacity: int | None = None,
+                    va_window: tuple[int, int] | None = None) -> EncodedStreams:
     """Encode the stream formed by the segments (device sections; the
-    reference ``encode`` of the gathered words, codec.py:299-321)."""
+    reference ``encode`` of the gathered words, codec.py:299-321).
+    ``va_window`` (see ``kv_va_window``) lets full tiles arrive through a
+    swizzled tensor map over that window (``sz_encode_segments_va``)."""
     lib = N.load_library()
     book = _need_book(config)
     params = _config_params(config, book)
@@ -90,8 +105,10 @@ def encode_segments(seg_addrs: torch.Tensor, seg_bytes: int, config: CodecConfig
 
     def run(cap):
         bufs = EncodeBuffers(n, config, cap, dev)
-        N.check(lib.sz_encode_segments(N.ptr(seg_addrs), n_segs, seg_bytes, params, bufs.struct(),
-                                       N.ptr(ws), ws.numel(), N.stream_handle()), "encode_segments")
+        lo, hi = va_window if va_window is not None else (0, 0)
+        N.check(lib.sz_encode_segments_va(N.ptr(seg_addrs), n_segs, seg_bytes, lo, hi, params,
+                                          bufs.struct(), N.ptr(ws), ws.numel(),
+                                          N.stream_handle()), "encode_segments")
         return bufs
 
     bufs = run(cap)
@@ -142,7 +159,8 @@ def encode_kv_blocks(kv_caches, block_ids: torch.Tensor, config: CodecConfig, *,
                      capacity: int | None = None) -> EncodedStreams:
     """Encode a request's KV blocks (all layers, layer-major) in place."""
     addrs, seg = kv_block_table(kv_caches, block_ids)
-    return encode_segments(addrs, seg, config, capacity=capacity)
+    return encode_segments(addrs, seg, config, capacity=capacity,
+                           va_window=kv_va_window(kv_caches))
 
 
 def decode_kv_blocks(streams: EncodedStreams, config: CodecConfig, codebook: ExponentCodebook,

@@ -3,7 +3,9 @@
 Llama-3.1-8B KV in a vLLM-style pool: 32 layers x [num_blocks, 2, 16, 8, 128]
 BF16 (64 KiB per block); a 32K-token request owns 2048 random blocks per
 layer (4 GiB).  Compares, device-timed (CUDA events, 3 warm-up + 10 timed):
-  paged encode   encode_kv_blocks (producer bulk-copies the blocks in place)
+  paged encode   encode_kv_blocks (full tiles through a 128B-swizzled tensor
+                 map over the caches' VA window, sz_encode_segments_va)
+  paged encode (bulk copies)  one 1-D bulk copy per block (sz_encode_segments)
   gather+encode  torch gather into a contiguous buffer, then encode
   paged decode   decode straight into another pool's blocks
   decode+scatter decode contiguous, then torch scatter into the blocks
@@ -48,10 +50,19 @@ i16 = [c.view(torch.int16) for c in caches]
 d16 = [c.view(torch.int16) for c in dst]
 
 
-def paged_encode():
+def paged_encode_bulk():
     N.check(lib.sz_encode_segments(N.ptr(addrs), addrs.numel(), seg, params, bufs.struct(),
                                    N.ptr(eng.enc_ws), eng.enc_ws.numel(), N.stream_handle()),
             "enc")
+
+
+win = paged.kv_va_window(caches)
+
+
+def paged_encode():
+    N.check(lib.sz_encode_segments_va(N.ptr(addrs), addrs.numel(), seg, win[0], win[1], params,
+                                      bufs.struct(), N.ptr(eng.enc_ws), eng.enc_ws.numel(),
+                                      N.stream_handle()), "enc")
 
 
 def gather_encode():
@@ -88,7 +99,8 @@ def timeit(fn, reps=10):
 
 eng.ensure_capacity(torch.cat([c[ids].reshape(-1) for c in i16]).view(torch.uint16))
 res = {}
-for name, fn in (("paged_encode", paged_encode), ("gather_then_encode", gather_encode),
+for name, fn in (("paged_encode", paged_encode), ("paged_encode_bulk_copies", paged_encode_bulk),
+                 ("gather_then_encode", gather_encode),
                  ("paged_decode", paged_decode), ("decode_then_scatter", decode_scatter)):
     t = timeit(fn)
     res[name + "_gbs"] = round(raw / t / 1e9, 1)

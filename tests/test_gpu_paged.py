@@ -75,6 +75,26 @@ def test_paged_sections_and_roundtrip(fmt_name, block_shape, rate, mode, chunk):
         assert not bool(_sel(c, mask.nonzero().reshape(-1).cuda()).view(torch.uint8).any())
 
 
+@pytest.mark.parametrize("fmt_name,block_shape", [
+    ("bf16", (2, 16, 8, 128)),   # 64 KiB blocks: one 256-row box per tile
+    ("bf16", (2, 4, 1, 64)),     # 1 KiB blocks: 32 eight-row boxes per tile
+    ("e5m2", (2, 16, 2, 128)),   # 8 KiB FP8 blocks
+])
+def test_paged_va_window_matches_bulk_copies(fmt_name, block_shape):
+    """The tensor-map path over the caches' VA window and the per-segment
+    1-D bulk copies produce the same sections."""
+    from paper_2605_01708_b200 import paged
+    m, fmt, caches, cfg = make(fmt_name, block_shape, 4, 64, 0.01)
+    ids = torch.randperm(64, generator=torch.Generator().manual_seed(3))[:45].cuda()
+    addrs, seg = paged.kv_block_table(caches, ids)
+    win = paged.kv_va_window(caches)
+    assert win is not None
+    a = paged.encode_segments(addrs, seg, cfg, va_window=win)
+    b = paged.encode_segments(addrs, seg, cfg)
+    assert a.n_escapes == b.n_escapes
+    assert dict(a.section_bytes()) == dict(b.section_bytes())
+
+
 def test_paged_rejects_bad_blocks():
     from paper_2605_01708_b200 import paged
     m, fmt, caches, cfg = make("bf16", (3, 16, 8, 128), 1, 8, 0.0016)   # 96 KiB: not 2^k
