@@ -1,31 +1,35 @@
 // sz_encode.cu — K2: SplitZip encoder for sm_100a.
 //
 // Replaces codec.py:299-321 (encode) and its byte-identical Quad64 variant
-// codec.py:324-401 (encode_quad).  Two kernels on one stream:
+// codec.py:324-401 (encode_quad).  Three kernels on one stream:
 //
 // K2a  encode_tiles — persistent, warp-specialised, one CTA per SM (20 warps):
 //   warp 16    PRODUCER claims 32 KiB tiles of input words (global counter)
-//                       and streams them into a 4-deep shared-memory ring with
-//                       1-D TMA bulk copies (cp.async.bulk -> UBLKCP),
-//                       completion counted on an mbarrier.
-//   warps 0-15 DENSE    per 32-byte slot (16 BF16 / 32 FP8 words): split the
-//                       fields with byte permutes, map exponents through the
-//                       shared-memory marked LUT (bit 4 = escape, encode_quad's
-//                       table codec.py:340-342), pack the 4-bit nibble / 3-bit
-//                       code plane and the sign|mantissa plane (byte plane /
-//                       3-4 bit LE stream), vector-store both; leave the slot's
-//                       escape bitmask (ballot-style) and compact
-//                       (element, raw exponent) records in shared memory.
+//                       and streams them into a 4-deep shared-memory ring by
+//                       TMA: a 128B-swizzled 2-D tensor-map box per full tile
+//                       (contiguous input, or paged input inside a known VA
+//                       window), else 1-D bulk copies; completion counted on
+//                       an mbarrier.
+//   warps 0-15 DENSE    per 32-byte slot (16 BF16 / 32 FP8 words): four
+//                       lane-table lookups per 4-element group
+//                       (t4[k][e] = code << CB*k | escape << 16+k, from the
+//                       marked LUT of encode_quad, codec.py:340-342) give the
+//                       packed 4-bit / 3-bit code group and its escape flags;
+//                       the sign|mantissa plane is gathered with permutes and
+//                       multiplies; both planes are vector-stored.  The slot's
+//                       escape bitmask and compact (element, raw exponent)
+//                       records stay in shared memory.
 //   warps 17-19 WRITER  per tile: popc of the slot masks + warp scan = the
 //                       tile-local escape order, per-chunk counts
 //                       (codec.py:292-295), escape records written in
 //                       ascending element order into the tile's scratch slot.
 //   No CTA ever waits for another, so the stream runs at HBM speed.
 // K2b  escape_gather — decoupled look-back prefix over the per-tile escape
-//   counts (a few hundred KB), then coalesced moves of every tile's records
-//   to their global ordinals in escape_positions / escape_values
-//   (codec.py:281-296); tiles whose escapes overflowed the scratch slot are
-//   re-derived from the input in element order.
+//   counts, then coalesced moves of every regular tile's records to their
+//   global ordinals in escape_positions / escape_values (codec.py:281-296);
+//   tiles whose escapes overflowed the scratch slot are listed for K2c.
+// K2c  escape_heavy — one CTA per listed tile re-derives its escapes from the
+//   input in element order.
 #include <cstdio>
 #include <cstdlib>
 
@@ -116,39 +120,6 @@ __device__ __forceinline__ uint32_t fsw_key(uint32_t row) {  // row = slot >> 5
 }
 __device__ __forceinline__ uint32_t fsw(uint32_t slot) { return slot ^ fsw_key(slot >> 5); }
 
-template <int FMT>
-__device__ __forceinline__ void split_group(const uint32_t (&x)[8], int g, uint32_t& e4,
-                                            uint32_t& a4) {
-  if constexpr (FMT == SZ_BF16) {
-    // Elements 4g..4g+3 live in words 2g, 2g+1 (two little-endian u16 each).
-    const uint32_t lo4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x6420);
-    const uint32_t hi4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x7531);
-    e4 = ((hi4 << 1) & 0xFEFEFEFEu) | ((lo4 >> 7) & 0x01010101u);
-    a4 = (hi4 & 0x80808080u) | (lo4 & 0x7F7F7F7Fu);
-  } else if constexpr (FMT == SZ_E5M2) {
-    e4 = (x[g] >> 2) & 0x1F1F1F1Fu;
-    a4 = ((x[g] >> 5) & 0x04040404u) | (x[g] & 0x03030303u);
-  } else {
-    e4 = (x[g] >> 3) & 0x0F0F0F0Fu;
-    a4 = ((x[g] >> 4) & 0x08080808u) | (x[g] & 0x07070707u);
-  }
-}
-
-// Four marked-LUT lookups.  Each byte index is extracted with one PRMT and
-// the LUT lives in static shared memory, so every lookup is PRMT + LDS with
-// an immediate base (no shift/mask/base-add sequence).
-// `lut` is 256-byte aligned, so the shared address of entry e is the LUT's
-// address with its low byte replaced by e: one PRMT builds it (byte k of e4
-// into byte 0, bytes 1-3 from the base) — no shift / mask / add.
-__device__ __forceinline__ uint32_t lut4(const uint8_t* lut, uint32_t e4) {
-  const uint32_t base = smem_addr(lut);
-  const uint32_t m0 = lds_u8(__byte_perm(e4, base, 0x7650));
-  const uint32_t m1 = lds_u8(__byte_perm(e4, base, 0x7651));
-  const uint32_t m2 = lds_u8(__byte_perm(e4, base, 0x7652));
-  const uint32_t m3 = lds_u8(__byte_perm(e4, base, 0x7653));
-  return __byte_perm(__byte_perm(m0, m1, 0x0040), __byte_perm(m2, m3, 0x0040), 0x5410);
-}
-
 // ---------------------------------------------------------------- T4 tables
 // Lane tables for 4-bit codes (the north-star configuration):
 //   t4[k][e] = code(e) << 4k  |  escape(e) << (16 + k)
@@ -177,7 +148,6 @@ constexpr int kT4Entries = (FMT == SZ_BF16 || (FMT == SZ_E5M2 && kE5FullByte)) ?
                            : (FMT == SZ_E5M2 ? 32 : 16);
 // Lane tables for every code width: with 3-bit codes the four lookups of a
 // group sum to its 12-bit code group (bits 0-11), flags still in bits 16-19.
-template <int FMT, int CB> constexpr bool kUseT4 = CB == 4 || CB == 3;
 
 template <int OFF>
 __device__ __forceinline__ uint32_t lds_u32_off(uint32_t saddr) {
@@ -280,118 +250,58 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
   constexpr int SBYTES = EPV * SMB / 8;
   constexpr int CWORDS = (CBYTES + 3) / 4;
   constexpr int SWORDS = (SBYTES + 3) / 4;
-  if constexpr (kUseT4<FMT, CB>) {
-    const uint32_t base = smem_addr(lut);  // the T4 tables (see t4_group)
-    uint32_t r[G];
-    uint32_t any = 0;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      r[g] = t4_group<FMT>(x, g, base, a.lut_stride, a.one);
-      if (TAIL && nv < EPV) {  // tail slot: no codes or flags beyond N (x is 0 there)
-        const int v = min(max(nv - 4 * g, 0), 4);
-        r[g] &= v >= 4 ? 0xFFFFFFFFu
-                       : (((1u << (CB * v)) - 1u) | (((1u << v) - 1u) << 16) |
-                          (((1u << (3 * v)) - 1u) << 20));
-      }
-      any |= r[g];
-    }
-    uint32_t fm = 0;
-    if (any & 0x000F0000u) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) fm |= ((r[g] >> 16) & 0xFu) << (4 * g);
-    }
-    uint32_t cw[CWORDS], sw[SWORDS];
-    if constexpr (CB == 4) {
-#pragma unroll
-      for (int i = 0; i < CWORDS; ++i) cw[i] = __byte_perm(r[2 * i], r[2 * i + 1], 0x5410);
-    } else {
-      uint32_t grp[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) grp[g] = r[g] & 0xFFFu;
-      concat_groups<G, 12>(grp, cw);
-    }
-    if constexpr (FMT == SZ_E4M3) {
-      uint32_t grp[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        grp[g] = pack_nib4(((x[g] >> 4) & 0x08080808u) | (x[g] & 0x07070707u));
-      concat_groups<G, 16>(grp, sw);
-    } else if constexpr (FMT == SZ_BF16) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const uint32_t lo4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x6420);
-        const uint32_t hi4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x7531);
-        sw[g] = bitselect(hi4, lo4, 0x80808080u);
-      }
-    } else {
-      // 12-bit SM groups in bits 20-31: of each lookup result (full-byte
-      // tables) or of e5m2_sm_hi
-      uint32_t h[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) h[g] = kE5FullByte ? r[g] : e5m2_sm_hi(x[g], a.k_lo, a.k_hi);
-      sw[0] = (h[0] >> 20) | ((h[1] >> 8) & 0x00FFF000u) | ((h[2] << 4) & 0xFF000000u);
-      sw[1] = (h[2] >> 28) | ((h[3] >> 16) & 0x0000FFF0u) | ((h[4] >> 4) & 0x0FFF0000u) |
-              ((h[5] << 8) & 0xF0000000u);
-      sw[2] = (h[5] >> 24) | ((h[6] >> 12) & 0x000FFF00u) | (h[7] & 0xFFF00000u);
-    }
-    if (!TAIL || nv == EPV) {
-      st_packed<CBYTES>(cdst, cw);
-      st_packed<SBYTES>(sdst, sw);
-    } else if (nv > 0) {
-      st_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, a.codes_len);
-      st_bytes_clipped<SBYTES>(a.sm, e0 * SMB / 8, sw, a.sm_len);
-    }
-    return fm;
-  }
-  uint32_t mk[G], ag[G];
+  const uint32_t base = smem_addr(lut);  // the T4 tables (see t4_group)
+  uint32_t r[G];
   uint32_t any = 0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    uint32_t e4, a4;
-    split_group<FMT>(x, g, e4, a4);
-    uint32_t m4 = lut4(lut, e4);
-    if (TAIL && nv < EPV) {  // tail slot: zero codes, flags and SM beyond N
+    r[g] = t4_group<FMT>(x, g, base, a.lut_stride, a.one);
+    if (TAIL && nv < EPV) {  // tail slot: no codes or flags beyond N (x is 0 there)
       const int v = min(max(nv - 4 * g, 0), 4);
-      const uint32_t keep = v >= 4 ? 0xFFFFFFFFu : ((1u << (8 * v)) - 1u);
-      m4 &= keep;
-      a4 &= keep;
+      r[g] &= v >= 4 ? 0xFFFFFFFFu
+                     : (((1u << (CB * v)) - 1u) | (((1u << v) - 1u) << 16) |
+                        (((1u << (3 * v)) - 1u) << 20));
     }
-    mk[g] = m4;
-    ag[g] = a4;
-    any |= m4;
+    any |= r[g];
   }
   uint32_t fm = 0;
-  if (any & 0x10101010u) {
+  if (any & 0x000F0000u) {
 #pragma unroll
-    for (int g = 0; g < G; ++g) fm |= flags4(mk[g]) << (4 * g);
+    for (int g = 0; g < G; ++g) fm |= ((r[g] >> 16) & 0xFu) << (4 * g);
   }
   uint32_t cw[CWORDS], sw[SWORDS];
-  {
-    uint32_t grp[G];
-    if constexpr (CB == 4) {
+  if constexpr (CB == 4) {
 #pragma unroll
-      for (int g = 0; g < G; ++g) grp[g] = pack_nib4(mk[g] & 0x0F0F0F0Fu);
-      concat_groups<G, 16>(grp, cw);
-    } else {
-#pragma unroll
-      for (int g = 0; g < G; ++g) grp[g] = pack_tri4(mk[g] & 0x07070707u);
-      concat_groups<G, 12>(grp, cw);
-    }
-  }
-  if constexpr (SMB == 8) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) sw[g] = ag[g];
+    for (int i = 0; i < CWORDS; ++i) cw[i] = __byte_perm(r[2 * i], r[2 * i + 1], 0x5410);
   } else {
     uint32_t grp[G];
-    if constexpr (SMB == 4) {
 #pragma unroll
-      for (int g = 0; g < G; ++g) grp[g] = pack_nib4(ag[g]);
-      concat_groups<G, 16>(grp, sw);
-    } else {
+    for (int g = 0; g < G; ++g) grp[g] = r[g] & 0xFFFu;
+    concat_groups<G, 12>(grp, cw);
+  }
+  if constexpr (FMT == SZ_E4M3) {
+    uint32_t grp[G];
 #pragma unroll
-      for (int g = 0; g < G; ++g) grp[g] = pack_tri4(ag[g]);
-      concat_groups<G, 12>(grp, sw);
+    for (int g = 0; g < G; ++g)
+      grp[g] = pack_nib4(((x[g] >> 4) & 0x08080808u) | (x[g] & 0x07070707u));
+    concat_groups<G, 16>(grp, sw);
+  } else if constexpr (FMT == SZ_BF16) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t lo4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x6420);
+      const uint32_t hi4 = __byte_perm(x[2 * g], x[2 * g + 1], 0x7531);
+      sw[g] = bitselect(hi4, lo4, 0x80808080u);
     }
+  } else {
+    // 12-bit SM groups in bits 20-31: of each lookup result (full-byte
+    // tables) or of e5m2_sm_hi
+    uint32_t h[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) h[g] = kE5FullByte ? r[g] : e5m2_sm_hi(x[g], a.k_lo, a.k_hi);
+    sw[0] = (h[0] >> 20) | ((h[1] >> 8) & 0x00FFF000u) | ((h[2] << 4) & 0xFF000000u);
+    sw[1] = (h[2] >> 28) | ((h[3] >> 16) & 0x0000FFF0u) | ((h[4] >> 4) & 0x0FFF0000u) |
+            ((h[5] << 8) & 0xF0000000u);
+    sw[2] = (h[5] >> 24) | ((h[6] >> 12) & 0x000FFF00u) | (h[7] & 0xFFF00000u);
   }
   if (!TAIL || nv == EPV) {
     st_packed<CBYTES>(cdst, cw);
@@ -401,6 +311,7 @@ __device__ __forceinline__ uint32_t encode_slot(const uint32_t (&x)[8], const ui
     st_bytes_clipped<SBYTES>(a.sm, e0 * SMB / 8, sw, a.sm_len);
   }
   return fm;
+
 }
 
 // Position of element `idx` in the escape-position stream (codec.py:289-295).
@@ -445,27 +356,21 @@ __global__ void __launch_bounds__(kEncThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint64_t n = a.n;
-  // 4-bit codes: T4 lane tables (t4_group); otherwise the 256-byte marked LUT
-  // (256-aligned: PRMT-built addresses in lut4).
-  __shared__ __align__(1024) uint32_t s_tab[kUseT4<FMT, CB> ? 4 * kT4Entries<FMT> : 64];
+  // T4 lane tables (t4_group), 1 KiB aligned: PRMT-built addresses
+  constexpr int TE = kT4Entries<FMT>;
+  __shared__ __align__(1024) uint32_t s_tab[4 * TE];
   const uint8_t* s_lut = reinterpret_cast<const uint8_t*>(s_tab);
-  if constexpr (kUseT4<FMT, CB>) {
-    constexpr int TE = kT4Entries<FMT>;
-    for (int i = tid; i < 4 * TE; i += kEncThreads) {
-      const int k = i / TE, e = i % TE;
-      if constexpr (FMT == SZ_E5M2 && kE5FullByte) {  // e is the whole byte here
-        const uint32_t m = p.enc_lut[(e >> 2) & 31];
-        const uint32_t a = ((e >> 5) & 4u) | (e & 3u);
-        s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k)) |
-                   (a << (20 + 3 * k));
-      } else {
-        const uint32_t m = p.enc_lut[e];
-        s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k));
-      }
+  for (int i = tid; i < 4 * TE; i += kEncThreads) {
+    const int k = i / TE, e = i % TE;
+    if constexpr (FMT == SZ_E5M2 && kE5FullByte) {  // e is the whole byte here
+      const uint32_t m = p.enc_lut[(e >> 2) & 31];
+      const uint32_t a = ((e >> 5) & 4u) | (e & 3u);
+      s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k)) |
+                 (a << (20 + 3 * k));
+    } else {
+      const uint32_t m = p.enc_lut[e];
+      s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k));
     }
-  } else {
-    for (int i = tid; i < 256; i += kEncThreads)
-      reinterpret_cast<uint8_t*>(s_tab)[i] = p.enc_lut[i];
   }
   if (blockIdx.x == 0 && tid == 0) *a.base_snapshot = a.escape_base ? *a.escape_base : 0;
   if (tid == 0) {
@@ -818,17 +723,13 @@ constexpr int kGatherUnroll = 4;
 template <int FMT, int POSB>
 __global__ void __launch_bounds__(kThreads)
     escape_gather(const __grid_constant__ sz_params p, const GatherArgs a) {
-  constexpr int PB = POSB == 0 ? 1 : POSB;
-  constexpr int WB = Fmt<FMT>::kWordBytes;
   __shared__ uint64_t tpref[kGatherTiles];
   __shared__ uint32_t tcnt[kGatherTiles];
   // group-relative prefix of the records K2b moves (regular tiles only; an
   // escape-heavy tile counts 0 here, K2c writes its records)
   __shared__ uint32_t rpref[kGatherTiles + 1];
   __shared__ unsigned long long s_group;
-  __shared__ uint8_t lut[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < 256; i += kThreads) lut[i] = p.enc_lut[i];
   // Tickets in launch order: group = ticket / R, part = ticket % R.  Part 0
   // runs the decoupled look-back and publishes; parts 1..R-1 only read the
   // predecessors' states (earlier tickets: forward progress) and move their
