@@ -14,6 +14,8 @@ Host outputs land directly in pinned buffers.
 from __future__ import annotations
 
 import math
+import os
+import time
 import warnings
 
 import numpy as np
@@ -27,6 +29,7 @@ from .formats import pack_bits_device
 
 PIECE_ELEMS = 1 << 26   # 128 MiB of BF16 per piece
 NBUF = 3                # device buffer sets in flight (H2D | kernel | D2H)
+_TRACE = bool(os.environ.get("SZ_HOSTPIPE_TRACE"))   # per-phase host timings (diagnostics)
 
 
 def piece_size(config: CodecConfig, n: int) -> int:
@@ -35,6 +38,28 @@ def piece_size(config: CodecConfig, n: int) -> int:
     if config.chunked and PIECE_ELEMS % config.chunk_size:
         p = config.chunk_size * max(1, PIECE_ELEMS // config.chunk_size)
     return p
+
+
+def piece_bounds(config: CodecConfig, n: int) -> list[tuple[int, int]]:
+    """Chunk-aligned [lo, hi) pieces: P/8, P/4, P/2 first, full P pieces, then
+    halving sizes at the end.  Short first and last pieces shorten the
+    pipeline's fill (H2D before any kernel can run) and drain (D2H after the
+    last kernel): each direction is busy for more of the call."""
+    P = piece_size(config, n)
+    unit = math.lcm(config.chunk_size, 64)   # chunk-aligned, whole bytes of every plane
+    floor = max(unit, (P // 8) // unit * unit)
+    ramp = [P // 8, P // 4, P // 2]
+    out, lo, i = [], 0, 0
+    while lo < n:
+        rem = n - lo
+        size = ramp[i] if i < len(ramp) else (max(rem // 2, floor) if rem <= 2 * P else P)
+        size = max(unit, size // unit * unit)
+        if size >= rem or rem - size < unit:
+            size = rem
+        out.append((lo, lo + size))
+        lo += size
+        i += 1
+    return out
 
 
 def pipelinable(config: CodecConfig, n: int) -> bool:
@@ -74,7 +99,7 @@ def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCo
     fmt = config.fmt
     n = words_h.numel()
     P = piece_size(config, n)
-    npieces = -(-n // P)
+    pieces = piece_bounds(config, n)
     params = _config_params(config, codebook)
     cap = min(n, capacity if capacity is not None else default_capacity(n))
     cb = config.code_bits
@@ -99,9 +124,8 @@ def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCo
     ev_h2d = [torch.cuda.Event() for _ in range(NBUF)]
     ev_enc = [torch.cuda.Event() for _ in range(NBUF)]
     ev_d2h = [torch.cuda.Event() for _ in range(NBUF)]
-    for i in range(npieces):
+    for i, (lo, hi) in enumerate(pieces):
         b = i % NBUF
-        lo, hi = i * P, min(n, (i + 1) * P)
         k = hi - lo
         with torch.cuda.stream(st.h2d):
             if i >= NBUF:
@@ -153,12 +177,14 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     """Decode host sections piecewise into a pinned CPU tensor.  Returns None
     when any piece reports corruption (the caller re-runs the monolithic
     decode, which raises with the reference's exact error order)."""
+    t_start = time.perf_counter()
     lib = N.load_library()
     dev = N.device()
     fmt = config.fmt
     n, m = int(streams.n_elements), int(streams.n_escapes)
     P = piece_size(config, n)
-    npieces = -(-n // P)
+    pieces = piece_bounds(config, n)
+    npieces = len(pieces)
     params = _config_params(config, codebook)
     cb = config.code_bits
     c = config.chunk_size
@@ -174,7 +200,7 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
         counts_h = host_tensor(counts_np.astype(np.uint32, copy=False), torch.uint32).pin_memory()
     # ordinal offset of every piece = escapes in the chunks before it: only
     # the piece boundaries are needed (one reduceat, no full prefix array)
-    bounds = np.arange(0, n, P) // c
+    bounds = np.array([lo for lo, _ in pieces], dtype=np.int64) // c
     per_piece = np.add.reduceat(counts_np, bounds, dtype=np.int64) if counts_np.size else \
         np.zeros(len(bounds), np.int64)
     piece_first = np.concatenate([[0], np.cumsum(per_piece)])
@@ -187,6 +213,7 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     ws = [torch.empty(lib.sz_decode_workspace_bytes(P, 0, params), dtype=torch.uint8, device=dev)
           for _ in range(NBUF)]
 
+    t_setup = time.perf_counter()
     st = _Streams()
     cur = torch.cuda.current_stream()
     for s in (st.h2d, st.comp, st.d2h):
@@ -200,9 +227,8 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     ev_dec = [torch.cuda.Event() for _ in range(NBUF)]
     ev_d2h = [torch.cuda.Event() for _ in range(NBUF)]
     pbytes = config.position_nbytes
-    for i in range(npieces):
+    for i, (lo, hi) in enumerate(pieces):
         b = i % NBUF
-        lo, hi = i * P, min(n, (i + 1) * P)
         k = hi - lo
         k0, k1 = lo // c, -(-hi // c)
         o0, o1 = int(piece_first[i]), int(piece_first[i + 1])
@@ -232,9 +258,14 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
             st.d2h.wait_event(ev_dec[b])
             out_h[lo:hi].copy_(words_d[b][:k], non_blocking=True)
             ev_d2h[b].record(st.d2h)
+    t_enq = time.perf_counter()
     cur.wait_stream(st.d2h)
     cur.wait_stream(st.comp)
     raw = status.cpu().numpy()
+    if _TRACE:
+        t_end = time.perf_counter()
+        print(f"[hostpipe] decode_host setup {1e3 * (t_setup - t_start):.1f} ms, enqueue "
+              f"{1e3 * (t_enq - t_setup):.1f} ms, wait {1e3 * (t_end - t_enq):.1f} ms", flush=True)
     # verdict words only: flags + first_inv[] (counts_total / marks_total are
     # informational and always set)
     verdict_bytes = 8 + 8 * N.NUM_CHECKS
