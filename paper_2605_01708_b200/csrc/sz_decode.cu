@@ -337,18 +337,21 @@ __device__ __forceinline__ uint32_t e5m2_sm_bytes(uint32_t v12) {
 // Escape values staged per tile, compact in ordinal order (the decode warp
 // finds a value as slot_first[slot] + rank within the slot's bitmap word);
 // tiles with more escapes read the rest straight from global memory.
-constexpr int kDecValCap = 1024;
+// E5M2 tiles hold 16384 elements: 2048 values cover escape-dense books
+// (7% of a tile); E4M3's larger sign|mantissa plane leaves no room for it.
+template <int FMT> constexpr int kDecValCap = FMT == SZ_E5M2 ? 2048 : 1024;
 constexpr uint32_t kNoEscape = 0xFFFFFFFFu;
 
 // Value of escape bit j of a slot: compact index = the slot's first index +
 // rank of bit j among the slot's escape bits (valid streams have ascending
 // ordinals in element order); beyond the staged capacity read global memory.
 // Corrupt streams (flagged elsewhere) only ever get a bounded read.
+template <int CAP>
 __device__ __forceinline__ uint32_t escape_value(const uint8_t* vals, uint32_t first,
                                                  uint32_t bm0, int j, uint64_t ofirst,
                                                  uint64_t m, const uint8_t* gvals) {
   const uint64_t c = static_cast<uint64_t>(first) + __popc(bm0 & ((1u << j) - 1u));
-  if (c < static_cast<uint64_t>(kDecValCap)) return vals[c];
+  if (c < static_cast<uint64_t>(CAP)) return vals[c];
   return ofirst + c < m ? gvals[ofirst + c] : 0u;
 }
 
@@ -361,7 +364,7 @@ __device__ __forceinline__ uint32_t escape_value(const uint8_t* vals, uint32_t f
 // steady state — only mbarrier hand-offs.
 constexpr int kDecHelpers = 3;                          // escape-staging warps
 constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
-constexpr int kDecOffStage = 256;                       // staged chunk offsets per helper
+constexpr int kDecOffStage = 64;                        // staged chunk offsets per helper
 template <int FMT>
 struct DecSmem {
   static constexpr int STAGES = 5;
@@ -371,7 +374,7 @@ struct DecSmem {
   alignas(128) uint8_t sm[STAGES][TILE * Fmt<FMT>::kSmBits / 8];
   uint32_t bitmap[STAGES][TILE / 32];
   uint32_t slot_first[STAGES][kDecSlots];  // compact index of a slot's first escape
-  uint8_t vals[STAGES][kDecValCap];        // escape values by (ordinal - ofirst)
+  uint8_t vals[STAGES][kDecValCap<FMT>];   // escape values by (ordinal - ofirst)
   uint64_t ofirst[STAGES];                 // ordinal of the tile's first escape
   uint64_t off[kDecHelpers][kDecOffStage + 1];
   uint64_t meta[STAGES];
@@ -506,7 +509,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         const uint32_t rel = static_cast<uint32_t>(idx - s0);
         atomicOr(&S.bitmap[s][rel >> 5], 1u << (rel & 31));
         atomicMin(&S.slot_first[s][rel / EPV], static_cast<uint32_t>(min(c, static_cast<uint64_t>(0xFFFFFFFEu))));
-        if (c < kDecValCap) S.vals[s][c] = static_cast<uint8_t>(v);
+        if (c < kDecValCap<FMT>) S.vals[s][c] = static_cast<uint8_t>(v);
       };
       uint64_t o_first = 0;
       if constexpr (ABS) {
@@ -553,7 +556,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
             else if (!in_book(v))
               record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-            if (o - t_first < kDecValCap) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
+            if (o - t_first < kDecValCap<FMT>) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
           }
         }
         mbar_wait(&S.full[s], ph);
@@ -873,8 +876,8 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           bm &= bm - 1;
           const uint32_t code = (pick<CWORDS>(cw, j >> 3) >> (4 * (j & 7))) & 0xF;
           if (!SENT && code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-          const uint32_t v = escape_value(S.vals[s], S.slot_first[s][slot], bm0, j, ofirst, m,
-                                          a.values);
+          const uint32_t v = escape_value<kDecValCap<FMT>>(S.vals[s], S.slot_first[s][slot], bm0,
+                                                           j, ofirst, m, a.values);
           const int g = j >> 2, sh = 8 * (j & 3);
 #pragma unroll
           for (int gg = 0; gg < G; ++gg)
@@ -937,8 +940,8 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           code = static_cast<uint32_t>(((hi << 32) | lo) >> (bit & 31)) & 7;
         }
         if (!SENT && code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-        const uint32_t v = escape_value(S.vals[s], S.slot_first[s][slot], bm0, j, ofirst, m,
-                                        a.values);
+        const uint32_t v = escape_value<kDecValCap<FMT>>(S.vals[s], S.slot_first[s][slot], bm0,
+                                                         j, ofirst, m, a.values);
         const int g = j >> 2, sh = 8 * (j & 3);
 #pragma unroll
         for (int gg = 0; gg < G; ++gg)
