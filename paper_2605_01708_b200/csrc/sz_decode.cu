@@ -172,7 +172,8 @@ __device__ __forceinline__ uint32_t slot_marks(const uint32_t* cw, int nv) {
 template <int FMT, int CB>
 __global__ void __launch_bounds__(kThreads)
     marks_kernel(const uint8_t* __restrict__ codes, uint64_t n, uint64_t codes_len,
-                 uint64_t num_tiles, uint32_t tile_slots, uint32_t* __restrict__ tile_marks) {
+                 uint64_t num_tiles, uint32_t tile_slots, uint32_t* __restrict__ tile_marks,
+                 uint32_t* __restrict__ mark_bits) {
   constexpr int EPV = kEpv<FMT>;
   constexpr int CBYTES = EPV * CB / 8;
   constexpr int CWORDS = (CBYTES + 3) / 4;
@@ -191,12 +192,22 @@ __global__ void __launch_bounds__(kThreads)
         uint4 v[kVec];
 #pragma unroll
         for (int i = 0; i < kVec; ++i) v[i] = __ldg(q + lane + 32 * i);
+        // 16 code bytes = 32 elements = one word of the element mark bitmap
+        uint32_t* const mb = mark_bits + t * tile_slots * EPV / 32;
 #pragma unroll
         for (int i = 0; i < kVec; ++i) {
           const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+          uint32_t word = 0;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            cnt += __popc(w4[k] & (w4[k] >> 1) & (w4[k] >> 2) & (w4[k] >> 3) & 0x11111111u);
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t f = w4[k] & (w4[k] >> 1) & (w4[k] >> 2) & (w4[k] >> 3) & 0x11111111u;
+            cnt += __popc(f);
+            uint32_t u = (f | (f >> 3)) & 0x03030303u;     // nibble flags -> 8 bits
+            u = (u | (u >> 6)) & 0x000F000Fu;
+            u = (u | (u >> 12)) & 0xFFu;
+            word |= u << (8 * k);
+          }
+          mb[lane + 32 * i] = word;
         }
 #pragma unroll
         for (int d = 16; d >= 1; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
@@ -216,7 +227,11 @@ __global__ void __launch_bounds__(kThreads)
       } else {
         ld_bytes_clipped<CBYTES>(codes, e0 * CB / 8, cw, codes_len);
       }
-      cnt += __popc(slot_marks<CB, EPV>(cw, nv));
+      const uint32_t mk = slot_marks<CB, EPV>(cw, nv);
+      cnt += __popc(mk);
+      const uint64_t slot_g = t * tile_slots + j;       // EPV-bit field of the bitmap
+      if constexpr (EPV == 32) mark_bits[slot_g] = mk;
+      else reinterpret_cast<uint16_t*>(mark_bits)[slot_g] = static_cast<uint16_t>(mk);
     }
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
@@ -272,6 +287,7 @@ struct DecodeArgs {
   // — decoded words go straight into the destination's KV-cache blocks.
   const uint64_t* seg_addrs;
   uint32_t seg_shift;
+  const uint32_t* mark_bits;  // sentinel: element mark bitmap from K3s
 };
 
 // Address of the 32-byte output slot starting at element e0 (slots never
@@ -559,40 +575,28 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             if (o - t_first < kDecValCap<FMT>) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
           }
         }
-        mbar_wait(&S.full[s], ph);
-        const uint32_t full_slots = static_cast<uint32_t>(min(n - s0, TILE) / EPV);
-        const uint32_t cbytes = (full_slots * CBYTES) & ~15u;
-        constexpr int SPL = kDecSlots / 32;  // consecutive slots per lane
-        uint32_t mk[SPL];
+        // The tile's marks come as K3s's element bitmap, loaded here right at
+        // the claim (no wait for the code plane's TMA): lane-contiguous words,
+        // one warp scan for the slots' first compact indices.
+        constexpr int SPL = kDecSlots / 32;      // consecutive slots per lane
+        constexpr int WPL = SPL * EPV / 32;      // their bitmap words
+        const uint4* mb = reinterpret_cast<const uint4*>(a.mark_bits + tile * (TILE / 32) +
+                                                         lane * WPL);
+        uint32_t wv[WPL];
+#pragma unroll
+        for (int i = 0; i < WPL / 4; ++i) {
+          const uint4 q = __ldg(mb + i);
+          wv[4 * i] = q.x; wv[4 * i + 1] = q.y; wv[4 * i + 2] = q.z; wv[4 * i + 3] = q.w;
+        }
+        const uint64_t valid = s1 - s0;          // elements of the (tail) tile
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) {
+          const uint64_t b0 = static_cast<uint64_t>(lane * WPL + k) * 32;
+          if (b0 + 32 > valid) wv[k] = b0 >= valid ? 0u : wv[k] & ((1u << (valid - b0)) - 1u);
+        }
         uint32_t cnt = 0;
 #pragma unroll
-        for (int j = 0; j < SPL; ++j) {
-          const uint32_t slot = lane * SPL + j;
-          const uint64_t e0 = s0 + static_cast<uint64_t>(slot) * EPV;
-          const int nv = e0 >= n ? 0 : (e0 + EPV <= n ? EPV : static_cast<int>(n - e0));
-          uint32_t cw[CWORDS];
-          if ((slot + 1) * CBYTES <= cbytes) {
-            const uint8_t* cp = S.codes[s] + slot * CBYTES;
-            if constexpr (CBYTES == 16) {
-              const uint4 v = *reinterpret_cast<const uint4*>(cp);
-              cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
-            } else if constexpr (CBYTES == 8) {
-              const uint2 v = *reinterpret_cast<const uint2*>(cp);
-              cw[0] = v.x; cw[1] = v.y;
-            } else if constexpr (CBYTES == 12) {
-              const uint32_t* q = reinterpret_cast<const uint32_t*>(cp);
-              cw[0] = q[0]; cw[1] = q[1]; cw[2] = q[2];
-            } else {
-              const uint16_t* q = reinterpret_cast<const uint16_t*>(cp);
-              cw[0] = q[0] | (static_cast<uint32_t>(q[1]) << 16);
-              cw[1] = q[2];
-            }
-          } else {
-            ld_bytes_clipped<CBYTES>(a.codes, e0 * CB / 8, cw, nv > 0 ? a.codes_len : 0);
-          }
-          mk[j] = nv > 0 ? slot_marks<CB, EPV>(cw, nv) : 0u;
-          cnt += __popc(mk[j]);
-        }
+        for (int k = 0; k < WPL; ++k) cnt += __popc(wv[k]);
         uint32_t incl = cnt;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -603,14 +607,12 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
         for (int j = 0; j < SPL; ++j) {
           const uint32_t slot = lane * SPL + j;
-          if (mk[j]) S.slot_first[s][slot] = run;
-          run += __popc(mk[j]);
-          if constexpr (EPV == 32) {
-            S.bitmap[s][slot] = mk[j];
-          } else if (j & 1) {
-            S.bitmap[s][slot >> 1] = mk[j - 1] | (mk[j] << 16);
-          }
+          const uint32_t mk = EPV == 32 ? wv[j] : (wv[j >> 1] >> (16 * (j & 1))) & 0xFFFFu;
+          if (mk) S.slot_first[s][slot] = run;
+          run += __popc(mk);
         }
+#pragma unroll
+        for (int k = 0; k < WPL; ++k) S.bitmap[s][lane * WPL + k] = wv[k];
       } else if constexpr (ABS) {
         // the tile's ordinal range from K3a (abs_bounds_kernel); clamped,
         // so a corrupt (unsorted) stream only ever costs bounded reads
@@ -991,6 +993,7 @@ struct DecodeWs {
   uint64_t* dec_states;
   unsigned long long* dec_counter;
   uint32_t* tile_marks;  // sentinel: marks per decode tile
+  uint32_t* mark_bits;   // sentinel: one bit per element (K3s), read by the stagers
   size_t zero_bytes;  // prefix of the workspace that must be zeroed
   size_t total;
 };
@@ -1014,8 +1017,13 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   w.zero_bytes = (otiles + dtiles + 2 + nbounds) * sizeof(uint64_t);
   w.offsets = b + otiles + dtiles + 2;  // (abs32 bounds: inside the zeroed prefix)
   w.tile_marks = reinterpret_cast<uint32_t*>(w.offsets + (nchunks ? nchunks + 1 : nbounds));
+  // (16-byte aligned: the stagers read it with vector loads)
+  const uintptr_t mb = reinterpret_cast<uintptr_t>(w.tile_marks + (p->sentinel ? dtiles : 0));
+  w.mark_bits = reinterpret_cast<uint32_t*>((mb + 15) & ~static_cast<uintptr_t>(15));
+  const uint64_t nbits_words = p->sentinel ? dtiles * (decode_tile_for(p->fmt) / 32) : 0;
   w.total = w.zero_bytes + (nchunks ? (nchunks + 1) * sizeof(uint64_t) : 0) +
-            (p->sentinel ? dtiles * sizeof(uint32_t) : 0) + 256;
+            (p->sentinel ? dtiles * sizeof(uint32_t) + 16 + nbits_words * sizeof(uint32_t) : 0) +
+            256;
   return w;
 }
 
@@ -1107,12 +1115,12 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
     const uint32_t slots = kDecSlots;
     const uint8_t* codes = static_cast<const uint8_t*>(in->d_codes);
     switch (p->fmt * 2 + (p->code_bits == 4)) {
-      case 0: marks_kernel<SZ_BF16, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
-      case 1: marks_kernel<SZ_BF16, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
-      case 2: marks_kernel<SZ_E5M2, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
-      case 3: marks_kernel<SZ_E5M2, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
-      case 4: marks_kernel<SZ_E4M3, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
-      default: marks_kernel<SZ_E4M3, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks); break;
+      case 0: marks_kernel<SZ_BF16, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks, w.mark_bits); break;
+      case 1: marks_kernel<SZ_BF16, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks, w.mark_bits); break;
+      case 2: marks_kernel<SZ_E5M2, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks, w.mark_bits); break;
+      case 3: marks_kernel<SZ_E5M2, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks, w.mark_bits); break;
+      case 4: marks_kernel<SZ_E4M3, 3><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks, w.mark_bits); break;
+      default: marks_kernel<SZ_E4M3, 4><<<g, kThreads, 0, s>>>(codes, n, clen, dtiles, slots, w.tile_marks, w.mark_bits); break;
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);
@@ -1158,6 +1166,7 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   a.status = d_status;
   a.states = w.dec_states;
   a.tile_counter = w.dec_counter;
+  a.mark_bits = w.mark_bits;
   a.num_tiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
   a.n_chunks = nchunks;
   a.codes_len = (n * p->code_bits + 7) / 8;
