@@ -23,94 +23,11 @@
 // check records its smallest offending ordinal/element in sz_decode_status;
 // the host raises CorruptionError in the reference's check order.
 #include "sz_common.cuh"
+#include "sz_scan.cuh"
 
 namespace sz {
 
-// ------------------------------------------------------------------ K3
-struct OffsetsArgs {
-  const uint64_t* m_ptr;
-  const uint32_t* counts;
-  uint64_t n_counts;
-  uint64_t m;
-  uint64_t* offsets;      // n_counts + 1 entries
-  uint64_t* states;
-  unsigned long long* tile_counter;
-  uint64_t num_tiles;
-  sz_decode_status* status;
-  int32_t sentinel;       // counts are per-tile sentinel marks (codec.py:459-467)
-};
-
-// counts per thread: 64 -> 16384 chunks per CTA, so the look-back chain of
-// this latency-bound scan is short (2^31 words at c=1024 -> 128 CTAs)
-constexpr int kOffItems = 64;
-
-__global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) {
-  __shared__ uint64_t warp_tot[kWarps];
-  __shared__ unsigned long long s_tile;
-  __shared__ uint64_t s_excl, s_total;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(a.tile_counter, 1ull);
-  __syncthreads();
-  const uint64_t tile = s_tile;
-  const uint64_t base = (tile * kThreads + tid) * kOffItems;
-  uint32_t v[kOffItems];
-  uint64_t sum = 0;
-  if (base + kOffItems <= a.n_counts && !(reinterpret_cast<uintptr_t>(a.counts) & 15)) {
-    const uint4* src = reinterpret_cast<const uint4*>(a.counts + base);
-#pragma unroll
-    for (int j = 0; j < kOffItems / 4; ++j) {
-      const uint4 q = __ldg(src + j);
-      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < kOffItems; ++j) v[j] = base + j < a.n_counts ? a.counts[base + j] : 0u;
-  }
-#pragma unroll
-  for (int j = 0; j < kOffItems; ++j) sum += v[j];
-  // block exclusive scan of per-thread sums (u64: corrupted counts may be huge)
-  uint64_t incl = sum;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint64_t o = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += o;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint64_t w = lane < kWarps ? warp_tot[lane] : 0, xw = w;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint64_t o = __shfl_up_sync(0xffffffffu, xw, d);
-      if (lane >= d) xw += o;
-    }
-    if (lane < kWarps) warp_tot[lane] = xw - w;
-    const uint64_t total = __shfl_sync(0xffffffffu, xw, 31);
-    const uint64_t ex = lookback_warp(a.states, tile, total);
-    if (lane == 0) {
-      s_excl = ex;
-      s_total = ex + total;
-    }
-  }
-  __syncthreads();
-  uint64_t run = s_excl + warp_tot[warp] + incl - sum;
-#pragma unroll
-  for (int j = 0; j < kOffItems; ++j) {
-    if (base + j < a.n_counts) a.offsets[base + j] = run;
-    run += v[j];
-  }
-  if (tile == a.num_tiles - 1 && tid == 0) {
-    a.offsets[a.n_counts] = s_total;
-    const uint64_t m = a.m_ptr ? *a.m_ptr : a.m;
-    if (a.sentinel) {
-      a.status->marks_total = s_total;
-      if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_SENTINEL_COUNT);
-    } else {
-      a.status->counts_total = s_total;
-      if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_COUNTS_TOTAL);
-    }
-  }
-}
+// K3 (offsets_kernel, chunk-offset scan): sz_scan.cuh
 
 // decode tile: kDecItems 32-byte slots per decode thread
 constexpr int kDecItems = 2;
@@ -981,10 +898,6 @@ constexpr int kDecodeItems = 2;
 uint64_t decode_tile_for(uint32_t fmt) {
   return static_cast<uint64_t>(kDecodeItems) * kThreads * (fmt == SZ_BF16 ? 16 : 32);
 }
-uint64_t offsets_tiles(uint64_t n_counts) {
-  const uint64_t per = static_cast<uint64_t>(kThreads) * kOffItems;
-  return (n_counts + per - 1) / per;
-}
 
 struct DecodeWs {
   uint64_t* offsets;
@@ -1014,8 +927,11 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   w.off_counter = reinterpret_cast<unsigned long long*>(b + otiles);
   w.dec_states = b + otiles + 1;
   w.dec_counter = reinterpret_cast<unsigned long long*>(b + otiles + 1 + dtiles);
-  w.zero_bytes = (otiles + dtiles + 2 + nbounds) * sizeof(uint64_t);
-  w.offsets = b + otiles + dtiles + 2;  // (abs32 bounds: inside the zeroed prefix)
+  // offsets start 16-byte aligned (the scan's vector stores; the workspace
+  // base is 256-aligned); abs32 bounds sit inside the zeroed prefix
+  const uint64_t off0 = (otiles + dtiles + 2 + 1) & ~1ull;
+  w.zero_bytes = (off0 + nbounds) * sizeof(uint64_t);
+  w.offsets = b + off0;
   w.tile_marks = reinterpret_cast<uint32_t*>(w.offsets + (nchunks ? nchunks + 1 : nbounds));
   // (16-byte aligned: the stagers read it with vector loads)
   const uintptr_t mb = reinterpret_cast<uintptr_t>(w.tile_marks + (p->sentinel ? dtiles : 0));
@@ -1146,6 +1062,15 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
     oa.tile_counter = w.off_counter;
     oa.num_tiles = offsets_tiles(ncounts);
     oa.status = d_status;
+    if (oa.num_tiles > 32) {
+      // many CTAs: reduce-then-scan (per-CTA sums in the look-back state
+      // array, unused then) instead of a look-back chain across CTAs
+      offsets_sums_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(
+          oa, w.off_states);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return sz_record_cuda(e);
+      oa.sums = w.off_states;
+    }
     offsets_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(oa);
     e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);

@@ -37,6 +37,7 @@
 #include <cudaTypedefs.h>   // comes from cudaGetDriverEntryPoint — no -lcuda)
 
 #include "sz_common.cuh"
+#include "sz_scan.cuh"
 
 namespace sz {
 
@@ -699,7 +700,9 @@ struct GatherArgs {
   uint8_t* values;
   uint64_t capacity;
   uint64_t* n_escapes;
-  uint64_t* states;
+  const uint64_t* tile_pref;      // exclusive escape prefix per tile (+ total), from the scan
+  uint64_t* scan_states;          // (the scan's look-back states and ticket, for its launch)
+  unsigned long long* scan_counter;
   unsigned long long* counter;
   uint64_t num_groups;
   uint32_t chunk;
@@ -769,9 +772,9 @@ __global__ void __launch_bounds__(kThreads)
       }
       if (lane == 31) rpref[kGatherTiles] = rincl;
     }
-    const uint64_t agg = __shfl_sync(0xffffffffu, incl, 31);
-    const uint64_t ex = part == 0 ? lookback_warp(a.states, group, agg)
-                                  : (group ? lookback_wide<8>(a.states, group) : 0);
+    // the group's first ordinal comes from the tile-prefix scan (K2b's
+    // separate single-pass scan kernel): no look-back inside this kernel
+    const uint64_t ex = a.tile_pref[t0];
     const uint64_t base = *a.base_snapshot;
     uint64_t run = base + ex + incl - lsum;
 #pragma unroll
@@ -781,8 +784,9 @@ __global__ void __launch_bounds__(kThreads)
       run += c[j];
     }
     if (lane == 0 && part == 0 && group == a.num_groups - 1) {
-      *a.n_escapes = ex + agg;
-      if (a.escape_base) *a.escape_base = base + ex + agg;
+      const uint64_t total = a.tile_pref[a.num_tiles];
+      *a.n_escapes = total;
+      if (a.escape_base) *a.escape_base = base + total;
     }
   }
   __syncthreads();
@@ -1084,7 +1088,9 @@ struct EncWs {
   unsigned long long* tile_counter;
   unsigned long long* gather_counter;
   uint64_t* snapshot;
-  uint64_t* states;
+  uint64_t* states;          // tile-prefix scan look-back states
+  unsigned long long* scan_counter;
+  uint64_t* tile_pref;
   uint32_t* tile_esc;
   uint8_t* scr_pos;
   uint8_t* scr_val;
@@ -1108,8 +1114,9 @@ EncWs carve(void* base, uint64_t n, const sz_params* p) {
   w.gather_counter = w.tile_counter + 1;
   w.snapshot = reinterpret_cast<uint64_t*>(w.tile_counter + 2);
   w.heavy_count = reinterpret_cast<unsigned int*>(w.tile_counter + 3);
-  w.states = reinterpret_cast<uint64_t*>(w.tile_counter + 4);
-  off = align256((4 + groups) * sizeof(uint64_t));
+  w.scan_counter = w.tile_counter + 4;
+  w.states = reinterpret_cast<uint64_t*>(w.tile_counter + 5);
+  off = align256((5 + offsets_tiles(tiles)) * sizeof(uint64_t));
   w.zero_bytes = off;
   w.tile_esc = reinterpret_cast<uint32_t*>(b + off);
   off = align256(off + tiles * sizeof(uint32_t));
@@ -1121,6 +1128,8 @@ EncWs carve(void* base, uint64_t n, const sz_params* p) {
   off = align256(off + tiles * sizeof(uint32_t));
   w.heavy_pref = reinterpret_cast<uint64_t*>(b + off);
   off = align256(off + tiles * sizeof(uint64_t));
+  w.tile_pref = reinterpret_cast<uint64_t*>(b + off);
+  off = align256(off + (tiles + 1) * sizeof(uint64_t));
   w.total = off;
   return w;
 }
@@ -1144,6 +1153,18 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
   kern<<<grid, kEncThreads, smem, s>>>(p, a, tm);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  {
+    OffsetsArgs oa{};
+    oa.counts = a.tile_esc;
+    oa.n_counts = a.num_tiles;
+    oa.offsets = const_cast<uint64_t*>(g.tile_pref);
+    oa.states = g.scan_states;
+    oa.tile_counter = g.scan_counter;
+    oa.num_tiles = offsets_tiles(a.num_tiles);
+    offsets_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(oa);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups * g.split), kThreads, 0, s>>>(p, g);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1290,7 +1311,9 @@ int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shi
   g.values = out->d_values;
   g.capacity = out->escape_capacity;
   g.n_escapes = out->d_n_escapes;
-  g.states = w.states;
+  g.tile_pref = w.tile_pref;
+  g.scan_states = w.states;
+  g.scan_counter = w.scan_counter;
   g.counter = w.gather_counter;
   g.num_groups = (a.num_tiles + kGatherTiles - 1) / kGatherTiles;
   g.chunk = a.chunk;
