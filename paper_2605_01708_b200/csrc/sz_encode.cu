@@ -795,7 +795,57 @@ __global__ void __launch_bounds__(kThreads)
   // prefixes), so all loads of the group are in flight at once.  Heavy
   // tiles' records are not visited at all (an all-heavy input leaves K2b
   // only its scan and the listing).
-  {
+  // Sparse groups (<= 32 records per tile on average) move tile by tile
+  // instead: a warp takes 4 tiles at a time, lane r moves record r of each —
+  // no per-record search (the flat pass's binary search made K2b
+  // instruction-bound at realistic escape rates).
+  auto move = [&](uint64_t src, uint64_t dst) {
+    a.values[dst] = a.scr_val[src];
+    if constexpr (POSB == 1) a.positions[dst] = a.scr_pos[src];
+    else if constexpr (POSB == 2)
+      reinterpret_cast<uint16_t*>(a.positions)[dst] = reinterpret_cast<const uint16_t*>(a.scr_pos)[src];
+    else if constexpr (POSB == 4)
+      reinterpret_cast<uint32_t*>(a.positions)[dst] = reinterpret_cast<const uint32_t*>(a.scr_pos)[src];
+  };
+  if (rpref[kGatherTiles] <= 32u * kGatherTiles) {
+    const int k_lo = static_cast<int>(kGatherTiles * part / a.split);
+    const int k_hi = static_cast<int>(kGatherTiles * (part + 1) / a.split);
+    constexpr int TU = 4;
+    for (int k0 = k_lo + warp * TU; k0 < k_hi; k0 += kWarps * TU) {
+      uint64_t src[TU], dst[TU];
+      uint32_t val[TU], pos[TU], cnt[TU];
+      bool live[TU];
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        const int k = k0 + u;
+        cnt[u] = k < k_hi ? tcnt[k] : 0u;   // 0 past the last tile of the stream
+        if (cnt[u] > kEscCap) cnt[u] = 0;     // heavy: K2c's
+        src[u] = (t0 + k) * kEscCap + lane;
+        dst[u] = (k < k_hi ? tpref[k] : 0) + lane;
+        live[u] = lane < cnt[u] && dst[u] < a.capacity;
+      }
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        if (!live[u]) continue;
+        val[u] = __ldg(a.scr_val + src[u]);
+        if constexpr (POSB == 1) pos[u] = __ldg(a.scr_pos + src[u]);
+        else if constexpr (POSB == 2) pos[u] = __ldg(reinterpret_cast<const uint16_t*>(a.scr_pos) + src[u]);
+        else if constexpr (POSB == 4) pos[u] = __ldg(reinterpret_cast<const uint32_t*>(a.scr_pos) + src[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        if (!live[u]) continue;
+        a.values[dst[u]] = static_cast<uint8_t>(val[u]);
+        if constexpr (POSB == 1) a.positions[dst[u]] = static_cast<uint8_t>(pos[u]);
+        else if constexpr (POSB == 2) reinterpret_cast<uint16_t*>(a.positions)[dst[u]] = static_cast<uint16_t>(pos[u]);
+        else if constexpr (POSB == 4) reinterpret_cast<uint32_t*>(a.positions)[dst[u]] = pos[u];
+      }
+#pragma unroll
+      for (int u = 0; u < TU; ++u)  // tiles with more than 32 records (rare here)
+        for (uint32_t r = lane + 32; r < cnt[u]; r += 32)
+          if (dst[u] - lane + r < a.capacity) move(src[u] - lane + r, dst[u] - lane + r);
+    }
+  } else {
     const uint64_t g_all = rpref[kGatherTiles];
     const uint64_t g_lo = g_all * part / a.split, g_hi = g_all * (part + 1) / a.split;
     const uint64_t g_total = g_hi - g_lo;
