@@ -365,9 +365,11 @@ def run_ours(args) -> None:
         "e2e": {"value": round(world * raw * e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                 "api": "paper_2605_01708_b200.encode/decode on pinned host words"},
-        # per step: K2a encode_tiles, K2b escape_gather, K2c escape_heavy
-        # (+ K6 pack_values for FP8), K3 offsets_kernel, K4 decode_persistent
-        "gpu_launches": K * (5 + (1 if fmt.exp_bits != 8 else 0)),
+        # per step: K2a encode_tiles, the tile-prefix scan, K2b escape_gather,
+        # K2c escape_heavy (+ K6 pack_values for FP8); K3 offsets (plus its
+        # per-CTA sums pass above 32 scan CTAs), K4 decode_persistent
+        "gpu_launches": K * (6 + (1 if fmt.exp_bits != 8 else 0) +
+                             (1 if scan_ctas(n_chunks_of(n, args.chunk)) > 32 else 0)),
         "calibration_histogram_gbs": round(hist_gbs, 1),
         "clocks": clocks,
     }
@@ -434,6 +436,15 @@ def cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m) -> dict:
                       f"({r['cpu_seconds']:.1f} CPU-s); numpy oracle of the reference codec",
             "encode_gbs": round(r["encode_gbs"], 4), "decode_gbs": round(r["decode_gbs"], 4),
             "slice_parity": "2^20-word prefix: GPU sections == oracle"}
+
+
+def n_chunks_of(n: int, chunk: int) -> int:
+    return -(-n // chunk)
+
+
+def scan_ctas(n_counts: int) -> int:
+    """CTAs of the offsets scan (sz_scan.cuh: 8192 counts per CTA)."""
+    return -(-n_counts // 8192)
 
 
 def wl_sm_bits(fmt_id: int) -> int:
