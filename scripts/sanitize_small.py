@@ -15,8 +15,9 @@ for fmt_id, fmt, bk, esc in ((0, sz.ElementFormat.BF16, O.BF16_BOOK, O.BF16_ESC)
             (0.0016, 1024, "explicit", "chunk", 4), (0.3, 256, "explicit", "chunk", 4),
             (0.01, 3000, "explicit", "chunk", 4), (0.01, 1024, "explicit", "abs32", 4),
             (0.01, 1024, "sentinel", "chunk", 4), (0.07, 1024, "explicit", "chunk", 3),
-            (0.3, 1024, "explicit", "abs32", 4)):
-        n = 200_003
+            (0.3, 1024, "explicit", "abs32", 4),
+            (0.01, 1, "explicit", "chunk", 4)):   # 300003 counts: multi-CTA reduce-then-scan
+        n = 300_003 if chunk == 1 else 200_003
         words = O.exact_stream(fmt_id, n, rate, 5, bk, esc)
         m = sz.CodebookMode.from_name(mode)
         book = tuple(e for e, _ in bk)[: (15 if mode == "sentinel" else (1 << bits))]
