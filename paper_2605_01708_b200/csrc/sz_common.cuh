@@ -298,6 +298,35 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* states, uint64_t til
   return excl;
 }
 
+// ------------------------------------------------ programmatic dependent launch
+// The codec's kernels run back to back on one stream (K2a -> scan -> K2b ->
+// K2c, then sums -> K3 -> K4).  Launched with programmatic stream
+// serialization (launch_pdl), a kernel's CTAs may be scheduled while its
+// predecessor's last CTAs still run: each kernel lets its dependents launch
+// at once (pdl_trigger) and waits for its predecessor's completion and
+// memory (pdl_wait) before its first global access; only the
+// shared-memory prologue overlaps.  Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // ------------------------------------------------ mbarrier + TMA bulk copy
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

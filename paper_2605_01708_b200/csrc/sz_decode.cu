@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
+  pdl_trigger();
   // Pair LUT in static shared memory, 1 KiB aligned: the address of entry i
   // is base | (i << 2), formed with one SHF + one LOP3 (no base add).
   __shared__ __align__(1024) uint32_t s_lut2[256];
@@ -380,6 +380,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     fence_barrier_init();
   }
   __syncthreads();
+  // the shared-memory prologue above only reads kernel parameters; from here
+  // on the predecessor grid's results are read
+  pdl_wait();
+  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
 
   if (warp == kWarps) {
     // ------------------------------------------------------------ producer
@@ -962,8 +966,8 @@ cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStrea
   if (per_sm < 1) per_sm = 1;
   const uint64_t want = static_cast<uint64_t>(sm_count()) * per_sm;
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
-  kern<<<grid, kDecThreads, smem, s>>>(p, a);
-  return cudaGetLastError();
+  e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, s, p, a);
+  return e == cudaSuccess ? cudaGetLastError() : e;
 }
 template <int FMT, int CB>
 cudaError_t dec_pos(int posb, const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
@@ -1065,14 +1069,15 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
     if (oa.num_tiles > 32) {
       // many CTAs: reduce-then-scan (per-CTA sums in the look-back state
       // array, unused then) instead of a look-back chain across CTAs
-      offsets_sums_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(
-          oa, w.off_states);
-      e = cudaGetLastError();
+      e = launch_pdl(offsets_sums_kernel, dim3(static_cast<unsigned>(oa.num_tiles)),
+                     dim3(kThreads), 0, s, oa, w.off_states);
+      if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess) return sz_record_cuda(e);
       oa.sums = w.off_states;
     }
-    offsets_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(oa);
-    e = cudaGetLastError();
+    e = launch_pdl(offsets_kernel, dim3(static_cast<unsigned>(oa.num_tiles)), dim3(kThreads), 0,
+                   s, oa);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
 

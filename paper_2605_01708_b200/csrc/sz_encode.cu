@@ -373,6 +373,8 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       s_tab[i] = ((m & ((1u << CB) - 1u)) << (CB * k)) | (((m >> 4) & 1u) << (16 + k));
     }
   }
+  pdl_trigger();
+  pdl_wait();  // (the tables above come from kernel parameters only)
   if (blockIdx.x == 0 && tid == 0) *a.base_snapshot = a.escape_base ? *a.escape_base : 0;
   if (tid == 0) {
     for (int s = 0; s < kEncInStages; ++s) {
@@ -732,11 +734,11 @@ __global__ void __launch_bounds__(kThreads)
   // escape-heavy tile counts 0 here, K2c writes its records)
   __shared__ uint32_t rpref[kGatherTiles + 1];
   __shared__ unsigned long long s_group;
+  pdl_trigger();
+  pdl_wait();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // Tickets in launch order: group = ticket / R, part = ticket % R.  Part 0
-  // runs the decoupled look-back and publishes; parts 1..R-1 only read the
-  // predecessors' states (earlier tickets: forward progress) and move their
-  // slice of the group's records — escape-dense inputs get R x the CTAs.
+  // Tickets: group = ticket / R, part = ticket % R; part p of a group moves
+  // its share of the group's records (escape-dense inputs get R x the CTAs).
   if (tid == 0) s_group = atomicAdd(a.counter, 1ull);
   __syncthreads();
   const uint64_t group = s_group / a.split;
@@ -934,6 +936,8 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t* const s_w = reinterpret_cast<uint32_t*>(heavy_smem);  // the round's words
   uint16_t* const s_idx = reinterpret_cast<uint16_t*>(heavy_smem + kThreads * 64);  // escapes
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_trigger();
+  pdl_wait();
   const unsigned int count = *a.heavy_count;
   if (blockIdx.x >= count) return;
   for (int i = tid; i < 4 * TB; i += kThreads)
@@ -1200,8 +1204,8 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
   if (e != cudaSuccess) return e;
   const uint64_t want = static_cast<uint64_t>(sm_count());
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
-  kern<<<grid, kEncThreads, smem, s>>>(p, a, tm);
-  e = cudaGetLastError();
+  e = launch_pdl(kern, dim3(grid), dim3(kEncThreads), smem, s, p, a, tm);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   {
     OffsetsArgs oa{};
@@ -1211,12 +1215,13 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
     oa.states = g.scan_states;
     oa.tile_counter = g.scan_counter;
     oa.num_tiles = offsets_tiles(a.num_tiles);
-    offsets_kernel<<<static_cast<unsigned>(oa.num_tiles), kThreads, 0, s>>>(oa);
-    e = cudaGetLastError();
+    e = launch_pdl(offsets_kernel, dim3(static_cast<unsigned>(oa.num_tiles)), dim3(kThreads), 0,
+                   s, oa);
     if (e != cudaSuccess) return e;
   }
-  escape_gather<FMT, POSB><<<static_cast<unsigned>(g.num_groups * g.split), kThreads, 0, s>>>(p, g);
-  e = cudaGetLastError();
+  e = launch_pdl(escape_gather<FMT, POSB>, dim3(static_cast<unsigned>(g.num_groups * g.split)),
+                 dim3(kThreads), 0, s, p, g);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // one wave of K2c CTAs (as many as fit per SM next to nothing else)
   static const int heavy_per_sm = [] {
@@ -1230,10 +1235,9 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
   }();
   if (heavy_per_sm <= 0) return cudaErrorInvalidConfiguration;
   const uint64_t heavy_grid = want * static_cast<uint64_t>(heavy_per_sm);
-  escape_heavy<FMT, POSB><<<static_cast<unsigned>(heavy_grid < a.num_tiles ? heavy_grid
-                                                                             : a.num_tiles),
-                             kThreads, kHeavySmem<FMT>, s>>>(p, g);
-  return cudaGetLastError();
+  return launch_pdl(escape_heavy<FMT, POSB>,
+                    dim3(static_cast<unsigned>(heavy_grid < a.num_tiles ? heavy_grid : a.num_tiles)),
+                    dim3(kThreads), kHeavySmem<FMT>, s, p, g);
 }
 
 template <int FMT, int CB>

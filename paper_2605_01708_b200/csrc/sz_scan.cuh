@@ -61,6 +61,8 @@ __device__ __forceinline__ void scan_load(const OffsetsArgs& a, uint64_t wbase,
 __global__ void __launch_bounds__(kThreads) offsets_sums_kernel(const OffsetsArgs a,
                                                                 uint64_t* sums) {
   __shared__ uint64_t wsum[kWarps];
+  pdl_trigger();
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t wbase = blockIdx.x * static_cast<uint64_t>(kScanPerCta) +
                          static_cast<uint64_t>(warp) * kScanPerWarp;
@@ -86,6 +88,8 @@ __global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) 
   __shared__ uint64_t warp_tot[kWarps];
   __shared__ unsigned long long s_tile;
   __shared__ uint64_t s_excl, s_total;
+  pdl_trigger();
+  pdl_wait();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (!a.sums) {
     if (tid == 0) s_tile = atomicAdd(a.tile_counter, 1ull);
