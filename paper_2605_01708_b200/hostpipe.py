@@ -214,6 +214,7 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
           for _ in range(NBUF)]
 
     t_setup = time.perf_counter()
+    _tr = {}
     st = _Streams()
     cur = torch.cuda.current_stream()
     for s in (st.h2d, st.comp, st.d2h):
@@ -227,11 +228,15 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     ev_dec = [torch.cuda.Event() for _ in range(NBUF)]
     ev_d2h = [torch.cuda.Event() for _ in range(NBUF)]
     pbytes = config.position_nbytes
+    if _TRACE:
+        _tr["pre"] = time.perf_counter() - t_setup
+        t_loop = time.perf_counter()
     for i, (lo, hi) in enumerate(pieces):
         b = i % NBUF
         k = hi - lo
         k0, k1 = lo // c, -(-hi // c)
         o0, o1 = int(piece_first[i]), int(piece_first[i + 1])
+        t_h0 = time.perf_counter()
         with torch.cuda.stream(st.h2d):
             if i >= NBUF:
                 st.h2d.wait_event(ev_dec[b])
@@ -241,6 +246,8 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
             sm_d[b][:s1 - s0].copy_(sm_h[s0:s1], non_blocking=True)
             cnt_d[b][:k1 - k0].copy_(counts_h[k0:k1], non_blocking=True)
             ev_h2d[b].record(st.h2d)
+        if _TRACE:
+            _tr["h2d"] = max(_tr.get("h2d", 0.0), time.perf_counter() - t_h0)
         st.comp.wait_event(ev_h2d[b])
         if i >= NBUF:
             st.comp.wait_event(ev_d2h[b])
@@ -251,21 +258,30 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
         src.d_values = (val_d.data_ptr() + o0) if o1 > o0 else None
         src.n_elements, src.n_escapes, src.n_counts = k, o1 - o0, k1 - k0
         src.d_n_escapes = None
+        t_k0 = time.perf_counter()
         N.check(lib.sz_decode(src, params, N.ptr(words_d[b]), N.ptr(status[i]), N.ptr(ws[b]),
                               ws[b].numel(), st.comp.cuda_stream), "decode")
+        if _TRACE:
+            _tr["kernel"] = max(_tr.get("kernel", 0.0), time.perf_counter() - t_k0)
         ev_dec[b].record(st.comp)
+        t_d0 = time.perf_counter()
         with torch.cuda.stream(st.d2h):
             st.d2h.wait_event(ev_dec[b])
             out_h[lo:hi].copy_(words_d[b][:k], non_blocking=True)
             ev_d2h[b].record(st.d2h)
+        if _TRACE:
+            _tr["d2h"] = max(_tr.get("d2h", 0.0), time.perf_counter() - t_d0)
     t_enq = time.perf_counter()
+    if _TRACE:
+        _tr["loop"] = t_enq - t_loop
     cur.wait_stream(st.d2h)
     cur.wait_stream(st.comp)
     raw = status.cpu().numpy()
     if _TRACE:
         t_end = time.perf_counter()
         print(f"[hostpipe] decode_host setup {1e3 * (t_setup - t_start):.1f} ms, enqueue "
-              f"{1e3 * (t_enq - t_setup):.1f} ms, wait {1e3 * (t_end - t_enq):.1f} ms", flush=True)
+              f"{1e3 * (t_enq - t_setup):.1f} ms, wait {1e3 * (t_end - t_enq):.1f} ms; max per piece "
+              + ", ".join(f"{k} {1e3 * v:.1f} ms" for k, v in _tr.items()), flush=True)
     # verdict words only: flags + first_inv[] (counts_total / marks_total are
     # informational and always set)
     verdict_bytes = 8 + 8 * N.NUM_CHECKS
