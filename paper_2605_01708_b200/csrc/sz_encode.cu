@@ -745,6 +745,10 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t part = static_cast<uint32_t>(s_group % a.split);
   const uint64_t t0 = group * kGatherTiles;
   if (warp == 0) {
+    // the group's first ordinal (tile-prefix scan) and the append base,
+    // loaded together with the tile counts: one memory latency, not two
+    const uint64_t ex = __ldg(a.tile_pref + t0);
+    const uint64_t base = *a.base_snapshot;
     // each lane owns kTilesPerLane consecutive tiles of the group
     constexpr int kTilesPerLane = kGatherTiles / 32;
     uint32_t c[kTilesPerLane];
@@ -774,10 +778,6 @@ __global__ void __launch_bounds__(kThreads)
       }
       if (lane == 31) rpref[kGatherTiles] = rincl;
     }
-    // the group's first ordinal comes from the tile-prefix scan (K2b's
-    // separate single-pass scan kernel): no look-back inside this kernel
-    const uint64_t ex = a.tile_pref[t0];
-    const uint64_t base = *a.base_snapshot;
     uint64_t run = base + ex + incl - lsum;
 #pragma unroll
     for (int j = 0; j < kTilesPerLane; ++j) {
