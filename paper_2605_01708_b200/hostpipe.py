@@ -84,11 +84,26 @@ def host_tensor(x, dtype: torch.dtype) -> torch.Tensor:
         return torch.from_numpy(arr)
 
 
-class _Streams:
+class _StreamSet:
     def __init__(self):
         self.h2d = torch.cuda.Stream()
         self.comp = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
+
+
+_STREAM_SETS: dict[int, _StreamSet] = {}
+
+
+def _Streams() -> _StreamSet:
+    """The pipeline's three streams, one fixed set per device: device memory
+    allocated under them (the escape sections' H2D) is then reused by the
+    caching allocator call after call — fresh pool streams each call made
+    every call allocate anew, and a cudaMalloc on this path measured up to
+    60 ms on some hosts."""
+    dev = torch.cuda.current_device()
+    if dev not in _STREAM_SETS:
+        _STREAM_SETS[dev] = _StreamSet()
+    return _STREAM_SETS[dev]
 
 
 def encode_host(words_h: torch.Tensor, config: CodecConfig, codebook: ExponentCodebook,
@@ -216,12 +231,18 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     t_setup = time.perf_counter()
     _tr = {}
     st = _Streams()
+    if _TRACE:
+        _tr["pre_streams"] = time.perf_counter() - t_setup
     cur = torch.cuda.current_stream()
     for s in (st.h2d, st.comp, st.d2h):
         s.wait_stream(cur)
+    if _TRACE:
+        _tr["pre_wait"] = time.perf_counter() - t_setup
     with torch.cuda.stream(st.h2d):
         pos_d = (host_tensor(streams.escape_positions, config.position_torch_dtype)
                  .to(dev, non_blocking=True) if m else None)
+        if _TRACE:
+            _tr["pre_pos"] = time.perf_counter() - t_setup
         val_d = host_tensor(streams.escape_values, torch.uint8).to(dev, non_blocking=True) \
             if m else None
     ev_h2d = [torch.cuda.Event() for _ in range(NBUF)]
