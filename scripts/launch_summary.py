@@ -14,9 +14,8 @@ for r in rows:
     name = r[4].split("(")[0].replace("void ", "")
     if skip and skip.search(name):
         continue
-    us = float(r[14].replace(",", "")) / (1000.0 if r[13] == "nsecond" else 1.0) if r[13] != "usecond" else float(r[14])
-    if r[13] == "msecond":
-        us = float(r[14]) * 1000
+    val = float(r[14].replace(",", ""))
+    us = {"nsecond": val / 1000.0, "usecond": val, "msecond": val * 1000.0}.get(r[13], val / 1000.0)
     tot[name] += us
     cnt[name] += 1
 all_us = sum(tot.values())
