@@ -137,11 +137,6 @@ __device__ __forceinline__ uint32_t pack_nib4(uint32_t b4) {
   uint32_t t = b4 | (b4 >> 4);
   return __byte_perm(t, 0, 0x4420);
 }
-// Four bytes, each < 8, to a 12-bit little-endian group (formats.py:184-189).
-__device__ __forceinline__ uint32_t pack_tri4(uint32_t b4) {
-  uint32_t u = (b4 | (b4 >> 5)) & 0x003F003Fu;
-  return (u | (u >> 10)) & 0xFFFu;
-}
 // Inverses.
 __device__ __forceinline__ uint32_t unpack_nib4(uint32_t x16) {
   uint32_t t = __byte_perm(x16, 0, 0x4140);
@@ -151,13 +146,6 @@ __device__ __forceinline__ uint32_t unpack_tri4(uint32_t x12) {
   uint32_t u = (x12 | (x12 << 10)) & 0x003F003Fu;
   return (u | (u << 5)) & 0x07070707u;
 }
-// Escape flags (bit 4 of each marked byte) of 4 elements -> 4-bit mask,
-// element 0 in bit 0.
-__device__ __forceinline__ uint32_t flags4(uint32_t marked4) {
-  uint32_t f = (marked4 >> 4) & 0x01010101u;
-  return (f * 0x01020408u) >> 24;
-}
-
 // Append G groups of W bits (W = 12 or 16) into a little-endian stream held
 // in `out` (ceil(G*W/32) words).
 template <int G, int W>
@@ -181,52 +169,6 @@ __device__ __forceinline__ uint32_t group_bits(const uint32_t* in, int g) {
   uint32_t v = in[wi] >> sh;
   if (sh + W > 32) v |= in[wi + 1] << (32 - sh);
   return v & ((1u << W) - 1);
-}
-
-// ------------------------------------------------------ block-wide scan
-// Exclusive scan of ITEMS x kThreads counts in (item, thread) order.
-// Returns the tile total; excl[i] receives this thread's prefix for item i.
-template <int ITEMS>
-struct BlockScanSmem {
-  uint32_t warp_tot[ITEMS * kWarps];
-  uint32_t total;
-};
-
-template <int ITEMS>
-__device__ __forceinline__ uint32_t block_scan(const uint32_t (&cnt)[ITEMS],
-                                               uint32_t (&excl)[ITEMS],
-                                               BlockScanSmem<ITEMS>& sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t incl[ITEMS];
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    uint32_t v = cnt[i];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane >= d) v += o;
-    }
-    incl[i] = v;
-    if (lane == 31) sm.warp_tot[i * kWarps + warp] = v;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    constexpr int kN = ITEMS * kWarps;
-    static_assert(kN <= 32, "scan spine must fit one warp");
-    uint32_t v = lane < kN ? sm.warp_tot[lane] : 0u;
-    uint32_t x = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= d) x += o;
-    }
-    if (lane < kN) sm.warp_tot[lane] = x - v;
-    if (lane == 31) sm.total = x;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) excl[i] = sm.warp_tot[i * kWarps + warp] + incl[i] - cnt[i];
-  return sm.total;
 }
 
 // ------------------------------------------------ decoupled look-back
@@ -399,9 +341,6 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
           "r"(smem_addr(dst)),
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
-}
-__device__ __forceinline__ void named_sync(uint32_t id, uint32_t threads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 // Atomic "keep the smallest index" into a zero-initialised slot, storing ~idx.
