@@ -142,7 +142,7 @@ def run_reference(args) -> None:
     book_w, esc = (BOOK16_BF16, ESC_BF16) if fmt == 0 else (BOOK16_E5M2, ESC_E5M2)
     book = tuple(e for e, _ in book_w)
     workers = max(1, min(os.cpu_count() or 1, 32))
-    per = 1 << 22
+    per = 1 << 24   # per process: 16 procs x 2^24 = the 2^28-word slice SURVEY §8(d) suggests
     for _ in range(args.warmup):
         cpu_bench.roundtrip_throughput(fmt, book, book_w, esc, args.escape_rate, args.chunk,
                                        per, workers, 1, seed=args.seed)
@@ -153,7 +153,7 @@ def run_reference(args) -> None:
         total_b += r["bytes"]
         total_t += r["wall_s"]
     gbs = total_b / total_t / 1e9
-    sample = (f"{workers} procs x 2^22 words per step (chunk-aligned shards of the {wl['name']} "
+    sample = (f"{workers} procs x 2^24 words per step (chunk-aligned shards of the {wl['name']} "
               "workload's exponent distribution), numpy oracle restating the reference codec")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
@@ -428,11 +428,11 @@ def cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m) -> dict:
     ok = cpu_bench.slice_parity(w, fmt_id, book.entries, args.chunk, sec)
     assert ok, "GPU sections differ from the oracle on the verification slice"
     workers = max(1, min(os.cpu_count() or 1, 32))
-    per = 1 << 22
+    per = 1 << 24   # 16 procs x 2^24 = a 2^28-word sample (~10-15 CPU-s)
     r = cpu_bench.roundtrip_throughput(fmt_id, book.entries, book_w, esc, args.escape_rate,
                                        args.chunk, per, workers, 1, seed=args.seed)
     return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": workers, "kind": "port",
-            "sample": f"{workers} procs x 2^22 words, one encode+decode each "
+            "sample": f"{workers} procs x 2^24 words, one encode+decode each "
                       f"({r['cpu_seconds']:.1f} CPU-s); numpy oracle of the reference codec",
             "encode_gbs": round(r["encode_gbs"], 4), "decode_gbs": round(r["decode_gbs"], 4),
             "slice_parity": "2^20-word prefix: GPU sections == oracle"}
