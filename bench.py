@@ -7,6 +7,11 @@ decode (K3+K4) of the rank's synthetic KV shard, inputs resident in HBM.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4]
                   [--chunk C] [--escape-rate E] [--impl ours|reference]
 
+``--gpus N`` with N > 1 outside torchrun re-launches itself under
+``torch.distributed.run`` with N local ranks (one per GPU, NCCL, rendezvous on
+127.0.0.1); under torchrun the rank count is WORLD_SIZE.  Rank 0 prints the
+line, with ``n_gpus`` = N, the whole-job aggregate and the per-rank spread.
+
 Workloads (BASELINE.json configs):
   c2  Llama-3.1-8B BF16 KV at 32K tokens per GPU (32 layers x K/V x 32768
       tokens x 8 KV heads x 128) = 2^31 words = 4 GiB.  Default.  Under
@@ -53,6 +58,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=20260517)
+    ap.add_argument("--elements", type=int, default=None,
+                    help="test only: elements per rank instead of the workload's "
+                         "(recorded in config.elements_override)")
     ap.add_argument("--no-handoff", action="store_true",
                     help="skip the N>=2 prefill->decode handoff leg (config 5)")
     return ap.parse_args()
@@ -189,6 +197,9 @@ def run_ours(args) -> None:
     backend = os.environ.get("SZ_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local % torch.cuda.device_count() if backend == "gloo" else local)
     local = torch.cuda.current_device()
+    if world > torch.cuda.device_count() and backend != "gloo":
+        raise SystemExit(f"--gpus {world}: only {torch.cuda.device_count()} CUDA device(s) "
+                         "visible (one rank per GPU)")
     if world > 1:
         if backend == "gloo":
             dist.init_process_group("gloo")
@@ -210,6 +221,8 @@ def run_ours(args) -> None:
     fmt = [sz.ElementFormat.BF16, sz.ElementFormat.FP8_E5M2][wl["fmt_id"]]
     book_w, esc = (BOOK16_BF16, ESC_BF16) if wl["fmt_id"] == 0 else (BOOK16_E5M2, ESC_E5M2)
     n = wl["n"]
+    if args.elements:
+        n = wl["n"] = int(args.elements)
     raw = n * fmt.word_nbytes
 
     # ---- input shard, generated on the device (K8)
@@ -268,6 +281,11 @@ def run_ours(args) -> None:
     enc_ms = sum(ev[k][0].elapsed_time(ev[k][1]) for k in range(K))
     dec_ms = sum(ev[k][1].elapsed_time(ev[k][2]) for k in range(K))
     tot_ms = ev[0][0].elapsed_time(ev[K - 1][2])
+    per_rank_ms = [tot_ms]
+    if world > 1:
+        got = [None] * world
+        dist.all_gather_object(got, tot_ms)
+        per_rank_ms = [float(x) for x in got]
     tot_ms = max_over_ranks(tot_ms)
     enc_ms = max_over_ranks(enc_ms)
     dec_ms = max_over_ranks(dec_ms)
@@ -351,8 +369,12 @@ def run_ours(args) -> None:
                    "code_bits": 4, "escape_rate_target": args.escape_rate,
                    "escape_rate": round(m / n, 6), "codebook": list(book.entries),
                    "l2": "inputs (>=2 GiB/rank) exceed the 126 MB L2; no flush needed",
-                   "step": "encode (K2) + decode (K3+K4), round trip"},
+                   "step": "encode (K2) + decode (K3+K4), round trip",
+                   **({"elements_override": n} if args.elements else {})},
         "encode_gbs": round(enc_gbs, 2), "decode_gbs": round(dec_gbs, 2),
+        "per_rank_gbs": {"min": round(raw * K / (max(per_rank_ms) / 1e3) / 1e9, 2),
+                         "max": round(raw * K / (min(per_rank_ms) / 1e3) / 1e9, 2),
+                         "backend": backend if world > 1 else None},
         "compression_ratio": round(raw / payload, 5),
         "vs_paper_b200": {"encode": round(enc_gbs / world / PAPER_B200["encode"], 3),
                           "decode": round(dec_gbs / world / PAPER_B200["decode"], 3)},
@@ -375,7 +397,8 @@ def run_ours(args) -> None:
     }
 
     if world >= 2 and world % 2 == 0 and not args.no_handoff and wl["fmt_id"] == 0:
-        line["handoff"] = handoff_leg(rank, world, raw_baseline=backend == "nccl")
+        line["handoff"] = handoff_leg(rank, world, raw_baseline=backend == "nccl",
+                                      n=min(1 << 30, n))
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m)
@@ -386,7 +409,7 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-def handoff_leg(rank: int, world: int, raw_baseline: bool = True) -> dict:
+def handoff_leg(rank: int, world: int, raw_baseline: bool = True, n: int = 1 << 30) -> dict:
     """Config 5 at N >= 2: pairs (2i -> 2i+1) hand 2 GiB of BF16 KV over in
     64 MiB pieces — raw NCCL P2P vs the fused encode -> peer-store -> decode
     link (peer.py) — for realistic and escape-heavy exponent statistics.
@@ -398,7 +421,7 @@ def handoff_leg(rank: int, world: int, raw_baseline: bool = True) -> dict:
     try:
         from bench_handoff import handoff_bench
         gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=120))
-        res = handoff_bench(1 << 30, 1 << 25, 3, False, rank, world, obj_group=gloo,
+        res = handoff_bench(n, min(1 << 25, n), 3, False, rank, world, obj_group=gloo,
                             timeout_s=20.0, raw_baseline=raw_baseline)
         res["pairs"] = world // 2
         res["unit"] = "GB/s of BF16 KV per pair (raw bytes / max device time over ranks)"
@@ -451,8 +474,32 @@ def wl_sm_bits(fmt_id: int) -> int:
     return {0: 8, 1: 3, 2: 4}[fmt_id]
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(n: int) -> int:
+    """``bench.py --gpus N`` run directly (no WORLD_SIZE in the environment):
+    re-run this command under torchrun with N local ranks, one per GPU, on a
+    127.0.0.1 rendezvous — the same launch the driver uses — and pass rank
+    0's JSON line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"[bench] WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -105,8 +105,11 @@ typedef struct sz_encoded_in {
   uint64_t n_counts;         /* length of d_counts as supplied              */
   /* Optional: when non-NULL the escape count M is read from this device
    * word (e.g. the encoder's d_n_escapes, or a received header) so a
-   * encode->transfer->decode pipeline needs no host round trip; n_escapes is
-   * then ignored and the caller guarantees positions/values hold M entries. */
+   * encode->transfer->decode pipeline needs no host round trip.  n_escapes
+   * is then the CAPACITY of d_positions / d_values (0 = they hold N entries):
+   * a device M above it is clamped for every read and reported as
+   * SZ_DEC_CAPACITY in the status flags, so an encoder overflow (M > K, see
+   * sz_encoded) never reads past the caller's escape buffers. */
   const uint64_t* d_n_escapes;
 } sz_encoded_in;
 
@@ -130,7 +133,10 @@ enum sz_decode_check {
   SZ_DEC_POS_NOT_INC = 10,  /* not strictly increasing           (codec.py:530-535) */
   SZ_DEC_CODE_RANGE = 11,   /* dense code >= n_entries           (codec.py:408-415) */
   SZ_DEC_NONDUMMY = 12,     /* escape carries a non-dummy code   (codec.py:472-476) */
-  SZ_DEC_NUM_CHECKS = 13
+  SZ_DEC_NUM_CHECKS = 13,
+  /* flag only (no first_inv slot): the device-resident M exceeds the escape
+   * capacity given in sz_encoded_in.n_escapes */
+  SZ_DEC_CAPACITY = 13
 };
 
 typedef struct sz_decode_status {

@@ -25,6 +25,7 @@ NUM_CHECKS = 13
 (DEC_CODE_PAD, DEC_SM_PAD, DEC_VALUE_DOMAIN, DEC_VALUE_IN_BOOK, DEC_SENTINEL_COUNT,
  DEC_ABS_PAST_END, DEC_ABS_NOT_INC, DEC_COUNTS_TOTAL, DEC_POS_OVER_CHUNK,
  DEC_POS_PAST_END, DEC_POS_NOT_INC, DEC_CODE_RANGE, DEC_NONDUMMY) = range(NUM_CHECKS)
+DEC_CAPACITY = 13   # flag only: device-resident M above the escape capacity
 
 
 class SzParams(C.Structure):

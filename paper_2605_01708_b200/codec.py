@@ -28,7 +28,7 @@ import torch
 from . import _native as N
 from .calibration import (CodebookMode, ExponentCodebook, build_histogram_device,
                           CalibrationStats, select_codebook)
-from .errors import ConfigError, CorruptionError, EmptyInputError
+from .errors import ConfigError, CorruptionError, EmptyInputError, NativeError
 from .formats import (ElementFormat, RawTensorStream, is_device, pack_bits_device,
                       packed_nbytes, to_device, to_numpy, trailing_bits_zero,
                       unpack_bits_device)
@@ -390,6 +390,21 @@ def _raise_values(first, streams, config):
                                               first[N.DEC_VALUE_IN_BOOK]))
 
 
+def _fetch_int(arr, i: int) -> int:
+    """One element of a host or device array (error messages only)."""
+    return int(to_numpy(arr[i:i + 1])[0])
+
+
+def _code_at(packed, el: int, code_bits: int) -> int:
+    """Dense code ``el`` of an LSB-first packed stream (formats.py:197-218);
+    reads the <= 2 bytes holding it, host or device."""
+    bit = el * code_bits
+    lo = bit >> 3
+    raw = to_numpy(packed[lo:lo + 2]).view(np.uint8)
+    word = int(raw[0]) | (int(raw[1]) << 8 if raw.size > 1 else 0)
+    return (word >> (bit & 7)) & ((1 << code_bits) - 1)
+
+
 def _counts_np(streams) -> np.ndarray | None:
     c = streams.chunk_counts
     return None if c is None else to_numpy(c).astype(np.int64)
@@ -408,6 +423,10 @@ def _raise_from_status(raw: np.ndarray, streams: EncodedStreams, config: CodecCo
                        codebook: ExponentCodebook, values_dev: torch.Tensor | None) -> None:
     st, first = _status_view(raw)
     flags = st.flags
+    if flags & (1 << N.DEC_CAPACITY):
+        raise NativeError("escape count M read on the device exceeds the decoder's escape "
+                          "capacity: re-run the encode with a larger capacity "
+                          "(DeviceCodec.ensure_capacity)")
     inconsistent = ((config.chunked and flags & (1 << N.DEC_COUNTS_TOTAL)) or
                     (config.sentinel and flags & (1 << N.DEC_SENTINEL_COUNT)))
     if inconsistent and values_dev is not None and streams.n_escapes:
@@ -436,14 +455,19 @@ def _raise_from_status(raw: np.ndarray, streams: EncodedStreams, config: CodecCo
         if flags & (1 << N.DEC_COUNTS_TOTAL):
             raise CorruptionError("chunk escape counts do not add up to the header total")
         counts = _counts_np(streams)
-        for chk, msg in ((N.DEC_POS_OVER_CHUNK, "escape position exceeds the chunk size"),
-                         (N.DEC_POS_PAST_END, "escape position beyond the end of the stream"),
+        o = first[N.DEC_POS_OVER_CHUNK]
+        if o is not None:
+            pos = _fetch_int(streams.escape_positions, o)
+            raise CorruptionError(f"escape position {pos} exceeds the chunk size",
+                                  chunk=_chunk_of(counts, config, o))
+        for chk, msg in ((N.DEC_POS_PAST_END, "escape position beyond the end of the stream"),
                          (N.DEC_POS_NOT_INC, "escape positions not strictly increasing")):
             if first[chk] is not None:
                 raise CorruptionError(msg, chunk=_chunk_of(counts, config, first[chk]))
     if first[N.DEC_CODE_RANGE] is not None:
         el = first[N.DEC_CODE_RANGE]
-        raise CorruptionError(f"dense code at element {el} exceeds the "
+        code = _code_at(streams.packed_codes, el, config.code_bits)
+        raise CorruptionError(f"dense code {code} at element {el} exceeds the "
                               f"{len(codebook.entries)}-entry codebook")
     if not config.sentinel and first[N.DEC_NONDUMMY] is not None:
         el = first[N.DEC_NONDUMMY]
@@ -468,10 +492,14 @@ def _pending_length_error(streams, config, n, m):
     return None
 
 
-def decode(streams: EncodedStreams, config: CodecConfig,
-           codebook: ExponentCodebook) -> RawTensorStream:
-    """Reconstruct the original words, validating every section
-    (codec.py:421-536); raises CorruptionError like the reference."""
+def check_section_lengths(streams: EncodedStreams, config: CodecConfig,
+                          codebook: ExponentCodebook) -> None:
+    """The host-side checks ``decode`` performs before launching
+    (codec.py:431-514): N >= 1, M <= N and every section length, raising
+    ``CorruptionError`` in the reference's priority order (a pad bit or an
+    escape value the reference checks before a failing length still wins).
+    Every entry point that launches the decode kernels on caller sections
+    calls this first, so the kernels never read past a short section."""
     fmt = config.fmt
     n, m = int(streams.n_elements), int(streams.n_escapes)
     if n < 1:
@@ -500,6 +528,15 @@ def decode(streams: EncodedStreams, config: CodecConfig,
             _, first = _status_view(status.cpu().numpy())
             _raise_values(first, streams, config)
         raise CorruptionError(msg)
+
+
+def decode(streams: EncodedStreams, config: CodecConfig,
+           codebook: ExponentCodebook) -> RawTensorStream:
+    """Reconstruct the original words, validating every section
+    (codec.py:421-536); raises CorruptionError like the reference."""
+    fmt = config.fmt
+    n, m = int(streams.n_elements), int(streams.n_escapes)
+    check_section_lengths(streams, config, codebook)
 
     if not is_device(streams.packed_codes):
         from . import hostpipe

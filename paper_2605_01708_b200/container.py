@@ -37,7 +37,7 @@ from .codec import (CodecConfig, EncodedStreams, PositionMode, _config_params, d
 from .errors import (BadMagicError, ConfigError, ContainerError, CorruptionError,
                      LengthMismatchError, TruncatedError, UnsupportedVersionError)
 from .formats import (ElementFormat, RawTensorStream, is_device, packed_nbytes,
-                      unpack_bits_device)
+                      trailing_bits_zero, unpack_bits_device)
 
 __all__ = [
     "CONTAINER_MAGIC", "RAW_MAGIC", "CODEBOOK_MAGIC", "FORMAT_VERSION",
@@ -103,8 +103,9 @@ class _Cursor:
 
 
 def _parse_codebook_record(cur: _Cursor) -> ExponentCodebook:
-    if cur.take(4, "codebook") != CODEBOOK_MAGIC:
-        raise BadMagicError("bad codebook magic")
+    magic = cur.take(4, "codebook")
+    if magic != CODEBOOK_MAGIC:
+        raise BadMagicError(f"bad codebook magic {magic!r}")
     version = cur.u8("codebook")
     if version != FORMAT_VERSION:
         raise UnsupportedVersionError(f"unsupported codebook version {version}")
@@ -219,10 +220,16 @@ def write_container(streams: EncodedStreams, config: CodecConfig,
 
 
 # ------------------------------------------------------------ parsing
+_VALUE_PAD_MSG = "nonzero padding bits in escape-value stream"
+
+
 def _unpack_values_np(raw: bytes, m: int, exp_bits: int) -> np.ndarray:
-    """Dense little-endian exp_bits stream -> raw values (codec.py:248-257)."""
+    """Dense little-endian exp_bits stream -> raw values (codec.py:248-257),
+    rejecting nonzero pad bits like the reference (codec.py:255-256)."""
     if exp_bits == 8:
         return np.frombuffer(raw, dtype=np.uint8).copy()
+    if not trailing_bits_zero(raw, m, exp_bits):
+        raise CorruptionError(_VALUE_PAD_MSG)
     bits = np.unpackbits(np.frombuffer(raw, dtype=np.uint8), bitorder="little")
     bits = bits[:m * exp_bits].reshape(m, exp_bits)
     return (bits.astype(np.uint8) << np.arange(exp_bits, dtype=np.uint8)).sum(
@@ -252,8 +259,9 @@ def container_from_bytes(data) -> tuple[EncodedStreams, CodecConfig, ExponentCod
         def fetch(lo, hi):
             return raw[lo:hi]
     cur = _Cursor(total, fetch)
-    if cur.take(4, "header") != CONTAINER_MAGIC:
-        raise BadMagicError("bad container magic")
+    magic = cur.take(4, "header")
+    if magic != CONTAINER_MAGIC:
+        raise BadMagicError(f"bad container magic {magic!r}")
     version = cur.u8("header")
     if version != FORMAT_VERSION:
         raise UnsupportedVersionError(f"unsupported container version {version}")
@@ -311,7 +319,9 @@ def container_from_bytes(data) -> tuple[EncodedStreams, CodecConfig, ExponentCod
         if fmt.exp_bits == 8:
             values = vals_packed
         elif m:
-            values, _ = unpack_bits_device(vals_packed, m, fmt.exp_bits)
+            values, pad_nonzero = unpack_bits_device(vals_packed, m, fmt.exp_bits)
+            if pad_nonzero:
+                raise CorruptionError(_VALUE_PAD_MSG)
         else:
             values = torch.empty(0, dtype=torch.uint8, device=buf.device)
         streams = EncodedStreams(
@@ -355,8 +365,9 @@ def raw_tensor_to_bytes(stream: RawTensorStream) -> bytes:
 def raw_tensor_from_bytes(data: bytes) -> RawTensorStream:
     data = bytes(data)
     cur = _Cursor(len(data), lambda lo, hi: data[lo:hi])
-    if cur.take(4, "header") != RAW_MAGIC:
-        raise BadMagicError("bad raw-tensor magic")
+    magic = cur.take(4, "header")
+    if magic != RAW_MAGIC:
+        raise BadMagicError(f"bad raw-tensor magic {magic!r}")
     version = cur.u8("header")
     if version != FORMAT_VERSION:
         raise UnsupportedVersionError(f"unsupported raw-tensor version {version}")

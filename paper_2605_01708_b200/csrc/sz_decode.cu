@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads)
     abs_bounds_kernel(const uint32_t* __restrict__ pos, const uint64_t* m_ptr, uint64_t m_host,
                       uint64_t n, uint64_t tile_elems, uint64_t num_tiles,
                       uint64_t* __restrict__ bounds) {
-  const uint64_t m = m_ptr ? min(*m_ptr, n) : m_host;
+  const uint64_t m = m_ptr ? min(*m_ptr, m_host) : m_host;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t first = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   auto tile_of = [&](uint64_t o) -> uint64_t {  // tile holding ordinal o's element
@@ -383,7 +383,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   // the shared-memory prologue above only reads kernel parameters; from here
   // on the predecessor grid's results are read
   pdl_wait();
-  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, n) : a.m;
+  const uint64_t n = a.n, m = a.m_ptr ? min(*a.m_ptr, a.m) : a.m;
+  if (a.m_ptr && blockIdx.x == 0 && tid == 0 && *a.m_ptr > a.m)
+    atomicOr(&a.status->flags, 1u << SZ_DEC_CAPACITY);
 
   if (warp == kWarps) {
     // ------------------------------------------------------------ producer
@@ -1008,7 +1010,11 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   if (!in || (!d_words_out && !seg_addrs) || !d_status || in->n_elements == 0)
     return SZ_ECONFIG;
   if (!in->d_n_escapes && in->n_escapes > in->n_elements) return SZ_ECONFIG;
-  const uint64_t n = in->n_elements, m = in->d_n_escapes ? n : in->n_escapes;
+  // device-resident M: n_escapes is the escape buffers' capacity (0 = N);
+  // every kernel reads min(*d_n_escapes, m)
+  const uint64_t n = in->n_elements;
+  const uint64_t m = in->d_n_escapes ? (in->n_escapes ? min(in->n_escapes, n) : n)
+                                     : in->n_escapes;
   if ((reinterpret_cast<uintptr_t>(d_words_out) & 31) ||
       (reinterpret_cast<uintptr_t>(in->d_codes) & 15) || (reinterpret_cast<uintptr_t>(in->d_sm) & 15))
     return SZ_EALIGN;

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) offsets_kernel(const OffsetsArgs a) 
   if (tile == a.num_tiles - 1 && tid == 0) {
     a.offsets[n] = s_total;
     if (a.status) {
-      const uint64_t m = a.m_ptr ? *a.m_ptr : a.m;
+      const uint64_t m = a.m_ptr ? min(*a.m_ptr, a.m) : a.m;
       if (a.sentinel) {
         a.status->marks_total = s_total;
         if (s_total != m) atomicOr(&a.status->flags, 1u << SZ_DEC_SENTINEL_COUNT);

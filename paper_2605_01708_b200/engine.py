@@ -30,7 +30,8 @@ class DeviceCodec:
         self.config, self.codebook, self.n = config, codebook, n
         self.device = device or N.device()
         self.params = _config_params(config, codebook)
-        self.capacity = min(n, capacity if capacity is not None else default_capacity(n))
+        self.capacity = max(1, min(n, capacity if capacity is not None
+                                       else default_capacity(n)))
         self.bufs = EncodeBuffers(n, config, self.capacity, self.device)
         self.enc_ws = torch.empty(self.lib.sz_encode_workspace_bytes(n, self.params),
                                   dtype=torch.uint8, device=self.device)
@@ -91,7 +92,9 @@ class DeviceCodec:
         src.n_elements = self.n
         src.n_counts = counts.numel() if counts is not None else 0
         if m is None:
-            src.n_escapes = 0
+            # device-resident M, clamped to what the escape buffers hold; a
+            # larger M (encoder overflow) raises in check_status
+            src.n_escapes = min(self.capacity, values.numel())
             src.d_n_escapes = N.ptr(b.m if m_dev is None else m_dev)
         else:
             src.n_escapes = m

@@ -28,7 +28,7 @@ import torch
 from . import _native as N
 from .calibration import ExponentCodebook
 from .codec import (CodecConfig, EncodeBuffers, EncodedStreams, _config_params,
-                    _raise_from_status, default_capacity)
+                    _raise_from_status, check_section_lengths, default_capacity)
 from .errors import ConfigError
 from .formats import packed_nbytes
 
@@ -132,6 +132,10 @@ def decode_segments(streams: EncodedStreams, config: CodecConfig, codebook: Expo
     if n * config.fmt.word_nbytes != seg_addrs.numel() * seg_bytes:
         raise ConfigError(f"{seg_addrs.numel()} segments of {seg_bytes} B do not hold "
                           f"{n} elements")
+    # the same length / pad / N / M checks decode performs before launching:
+    # a section shorter than the header says must raise here, never be read
+    # past by the kernel that writes into live KV blocks
+    check_section_lengths(streams, config, codebook)
     params = _config_params(config, codebook)
     dev = seg_addrs.device
     codes = to_device(streams.packed_codes, torch.uint8, align=16)

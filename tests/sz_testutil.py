@@ -71,3 +71,47 @@ def oracle_params(case: dict):
     from oracle import sz_oracle as O
     return O.Params(case["fmt"], case["code_bits"], case["sentinel"], case["chunk"],
                     case["abs32"])
+
+
+class Robust:
+    """Lazy view over tests/golden/{robust.npz,robust.json.gz}: the reference's
+    verdicts on mutated containers (tests/golden/make_robustness.py)."""
+
+    def __init__(self):
+        import gzip
+        with gzip.open(GOLDEN_DIR / "robust.json.gz", "rb") as f:
+            meta = json.loads(f.read())
+        self.bases = meta["bases"]
+        self.verdicts = meta["verdicts"]
+        self._npz = np.load(GOLDEN_DIR / "robust.npz")
+        self._cache: dict[str, tuple[bytes, np.ndarray]] = {}
+
+    def base(self, bid: str) -> tuple[bytes, np.ndarray]:
+        if bid not in self._cache:
+            self._cache[bid] = (self._npz[f"{bid}/container"].tobytes(),
+                                self._npz[f"{bid}/words"])
+        return self._cache[bid]
+
+    def mutated(self, v: dict) -> bytes:
+        data, _ = self.base(v["base"])
+        if v["kind"] == "truncate":
+            return data[:v["mut"]]
+        pos, x = v["mut"]
+        b = bytearray(data)
+        b[pos] ^= x
+        return bytes(b)
+
+
+_ROBUST = None
+
+
+def robust() -> Robust:
+    global _ROBUST
+    if _ROBUST is None:
+        _ROBUST = Robust()
+    return _ROBUST
+
+
+def words_digest(words: np.ndarray) -> str:
+    import hashlib
+    return hashlib.blake2b(np.ascontiguousarray(words).tobytes(), digest_size=16).hexdigest()

@@ -62,6 +62,11 @@ def test_paged_sections_and_roundtrip(fmt_name, block_shape, rate, mode, chunk):
     enc = paged.encode_kv_blocks(caches, ids, cfg)
     assert enc.n_escapes == ref.n_escapes
     assert dict(enc.section_bytes()) == dict(ref.section_bytes())
+    # and both equal the CPU oracle's encode of the gathered words
+    from oracle import sz_oracle as O
+    p = O.Params({"bf16": 0, "e5m2": 1}[fmt_name], 4, mode == "sentinel", chunk, False)
+    osec = O.encode(gathered.cpu().numpy(), p, tuple(cfg.codebook.entries))
+    assert [b for _, b in enc.section_bytes()] == O.section_bytes(osec)
     # decode into a different pool with a different block table
     dst = [torch.zeros_like(c) for c in caches]
     ids2 = torch.randperm(40, generator=g)[:23].cuda()
@@ -135,3 +140,50 @@ def test_concurrent_encodes_on_two_streams_do_not_interfere():
     assert dict(e1.streams().section_bytes()) == ref1
     assert dict(e2.streams().section_bytes()) == ref2
     assert torch.equal(e1.out, w1) and torch.equal(e2.out, w2)
+
+
+def test_decode_segments_checks_section_lengths():
+    """decode_segments raises CorruptionError like decode on sections that
+    contradict the header, before any kernel writes into live blocks."""
+    import dataclasses
+    from paper_2605_01708_b200 import paged
+    m, fmt, caches, cfg = make("bf16", (2, 16, 8, 128), 2, 16, 0.01)
+    ids = torch.arange(8, device="cuda")
+    enc = paged.encode_kv_blocks(caches, ids, cfg)
+    dst = [torch.zeros_like(c) for c in caches]
+    cases = {
+        "codes": dataclasses.replace(enc, packed_codes=enc.packed_codes[:-1]),
+        "sm": dataclasses.replace(enc, sign_mantissa=enc.sign_mantissa[:-1]),
+        "values": dataclasses.replace(enc, escape_values=enc.escape_values[:-1]),
+        "positions": dataclasses.replace(enc, escape_positions=enc.escape_positions[:-1]),
+        "counts": dataclasses.replace(enc, chunk_counts=enc.chunk_counts[:-1]),
+        "m_gt_n": dataclasses.replace(enc, n_escapes=enc.n_elements + 1),
+    }
+    for name, bad in cases.items():
+        with pytest.raises(m.CorruptionError):
+            paged.decode_kv_blocks(bad, cfg, enc.codebook, dst, ids)
+        for c in dst:
+            assert not bool(c.view(torch.uint8).any()), name
+
+
+def test_engine_device_m_is_clamped_to_capacity():
+    """DeviceCodec with a capacity below the input's escape count: the
+    decoder (M read on the device) never reads past the escape buffers and
+    check_status raises instead of returning wrong words."""
+    import paper_2605_01708_b200 as m
+    from paper_2605_01708_b200.engine import DeviceCodec, synth_kv
+    fmt = m.ElementFormat.BF16
+    n = 1 << 20
+    book = m.ExponentCodebook(fmt, tuple(e for e, _ in BF16_BOOK), 4,
+                              m.CodebookMode.TOPK_EXPLICIT)
+    eng = DeviceCodec(m.CodecConfig(fmt, codebook=book), book, n, capacity=64)
+    w = synth_kv(n, fmt, 4, BF16_BOOK, BF16_ESC, 0.05)
+    eng.encode(w)
+    eng.decode()
+    assert eng.n_escapes() > 64
+    with pytest.raises(m.NativeError, match="capacity"):
+        eng.check_status()
+    eng.ensure_capacity(w)
+    eng.decode()
+    eng.check_status()
+    assert torch.equal(eng.out, w)
