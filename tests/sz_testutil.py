@@ -115,3 +115,65 @@ def robust() -> Robust:
 def words_digest(words: np.ndarray) -> str:
     import hashlib
     return hashlib.blake2b(np.ascontiguousarray(words).tobytes(), digest_size=16).hexdigest()
+
+
+class RealKV:
+    """Real attention K/V dumps (kv_extractor's offline random-gpt2,
+    tests/golden/make_realkv.py) and the reference's results on them.
+    BF16 words come from the committed .szrw files; the E5M2 words are the
+    FP8 KV-cache cast of the same activations, rebuilt here and checked
+    against the reference's SHA-256."""
+
+    CONFIGS = {  # name -> (code_bits, sentinel, chunk, abs32, shared book key)
+        "dyn4": (4, False, 1024, False, None),
+        "cal4": (4, False, 1024, False, "4_explicit"),
+        "cal4_c256": (4, False, 256, False, "4_explicit"),
+        "cal3": (3, False, 1024, False, "3_explicit"),
+        "cal4_sent": (4, True, 1024, False, "4_sentinel"),
+        "cal4_abs32": (4, False, 1024, True, "4_explicit"),
+    }
+
+    def __init__(self):
+        self.dir = GOLDEN_DIR / "realkv"
+        self.ref = json.loads((GOLDEN_DIR / "realkv.json").read_text())
+        self._words: dict[tuple[str, str], np.ndarray] = {}
+
+    def files(self) -> list[str]:
+        return [d["file"] for d in self.ref["formats"]["bf16"]["dumps"]]
+
+    def dump(self, fmt: str, file: str) -> dict:
+        return next(d for d in self.ref["formats"][fmt]["dumps"] if d["file"] == file)
+
+    def calibrate(self, fmt: str) -> dict:
+        return self.ref["formats"][fmt]["calibrate"]
+
+    def words(self, fmt: str, file: str) -> np.ndarray:
+        key = (fmt, file)
+        if key not in self._words:
+            data = (self.dir / file).read_bytes()
+            n = int.from_bytes(data[6:14], "little")
+            bf16 = np.frombuffer(data, dtype="<u2", count=n, offset=14).copy()
+            if fmt == "bf16":
+                self._words[key] = bf16
+            else:
+                import torch
+                t = torch.from_numpy(bf16.view(np.int16)).view(torch.bfloat16)
+                self._words[key] = t.to(torch.float8_e5m2).view(torch.uint8).numpy().copy()
+        return self._words[key]
+
+
+_REALKV = None
+
+
+def realkv() -> RealKV:
+    global _REALKV
+    if _REALKV is None:
+        _REALKV = RealKV()
+    return _REALKV
+
+
+def sha256(b) -> str:
+    import hashlib
+    if isinstance(b, np.ndarray):
+        b = np.ascontiguousarray(b).tobytes()
+    return hashlib.sha256(bytes(b)).hexdigest()
