@@ -139,39 +139,69 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
+def bench_config(wl: dict, args, n: int, book_entries) -> dict:
+    """The ``config`` object both arms print (identical keys and values)."""
+    return {"workload": wl["desc"], "elements_per_gpu": n, "chunk": args.chunk,
+            "code_bits": 4, "escape_rate_target": args.escape_rate,
+            "codebook": [int(e) for e in book_entries],
+            "l2": "inputs (>=2 GiB/rank) exceed the 126 MB L2; no flush needed",
+            "step": "encode (K2) + decode (K3+K4), round trip",
+            **({"elements_override": n} if args.elements else {})}
+
+
+CPU_WORDS_PER_PROC = 1 << 25   # 16 procs x 2^25 = a quarter of c2's 2^31 words
+
+
+def oracle_pool(wl: dict, args, book_entries, book_w, esc):
+    from oracle import cpu_bench
+    workers = max(1, min(os.cpu_count() or 1, 32))
+    return cpu_bench.OraclePool(wl["fmt_id"], book_entries, book_w, esc, args.escape_rate,
+                                args.chunk, CPU_WORDS_PER_PROC, workers, seed=args.seed)
+
+
 def run_reference(args) -> None:
+    """``--impl reference``: the reference's algorithm (the numpy oracle port,
+    >= the reference's per-core speed) on every host core, one resident
+    chunk-aligned shard per process, each step one encode + decode of all
+    shards."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    from oracle import cpu_bench
     wl = workload(args.workload, world)
     fmt = wl["fmt_id"]
+    n = int(args.elements) if args.elements else wl["n"]
     book_w, esc = (BOOK16_BF16, ESC_BF16) if fmt == 0 else (BOOK16_E5M2, ESC_E5M2)
-    book = tuple(e for e, _ in book_w)
-    workers = max(1, min(os.cpu_count() or 1, 32))
-    per = 1 << 24   # per process: 16 procs x 2^24 = the 2^28-word slice SURVEY §8(d) suggests
-    for _ in range(args.warmup):
-        cpu_bench.roundtrip_throughput(fmt, book, book_w, esc, args.escape_rate, args.chunk,
-                                       per, workers, 1, seed=args.seed)
-    total_b = total_t = 0.0
-    for s in range(args.steps):
-        r = cpu_bench.roundtrip_throughput(fmt, book, book_w, esc, args.escape_rate, args.chunk,
-                                           per, workers, 1, seed=args.seed + s)
-        total_b += r["bytes"]
-        total_t += r["wall_s"]
+    # the bench's calibrated book: top 16 of the exponent distribution
+    book = tuple(e for e, _ in sorted(book_w, key=lambda t: -t[1]))
+    with oracle_pool(wl, args, book, book_w, esc) as pool:
+        one = pool.one_core()
+        for _ in range(args.warmup):
+            pool.step()
+        total_b = total_t = 0.0
+        for _ in range(args.steps):
+            r = pool.step()
+            total_b += r["bytes"]
+            total_t += r["wall_s"]
+        workers = pool.workers
     gbs = total_b / total_t / 1e9
-    sample = (f"{workers} procs x 2^24 words per step (chunk-aligned shards of the {wl['name']} "
-              "workload's exponent distribution), numpy oracle restating the reference codec")
+    sample = (f"{workers} procs x 2^{CPU_WORDS_PER_PROC.bit_length() - 1} words per step "
+              f"({workers * CPU_WORDS_PER_PROC / n:.3g} of the {wl['name']} workload, "
+              "chunk-aligned shards with its exponent distribution, resident in each "
+              "process); numpy oracle restating the reference codec")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total_t / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": wl["scaling"], "vs_baseline": None, "dtype": "u16" if fmt == 0 else "u8",
-        "data": "synthetic", "config": {"workload": wl["desc"], "chunk": args.chunk,
-                                        "escape_rate": args.escape_rate},
+        "data": "synthetic", "config": bench_config(wl, args, n, book),
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": workers, "kind": "port",
-                         "sample": sample},
+                         "sample": sample,
+                         "one_core": {"value": round(one["gbs"], 4), "cores": 1,
+                                      "encode_gbs": round(one["encode_gbs"], 4),
+                                      "decode_gbs": round(one["decode_gbs"], 4),
+                                      "sample": f"1 proc x 2^{CPU_WORDS_PER_PROC.bit_length() - 1}"
+                                                " words, one encode + decode"}},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -343,19 +373,26 @@ def run_ours(args) -> None:
     dom_ms = max(enc_launch_ms, dec_launch_ms)
     achieved = alg_bytes / (dom_ms / 1e3) / 1e9
     # DRAM traffic of the dominant kernel from the committed `ncu --set full`
-    # capture (profiles/ncu_traffic_<workload>_r*.json, bytes per element),
-    # scaled to this launch's element count.
-    traffic = None
+    # capture (profiles/ncu_traffic_<workload>_r*.json).  A capture taken at
+    # this launch's element count (scripts/gpu_prof_bench.sh runs ncu on
+    # scripts/profile_kernels.py at the bench's size) is used as measured;
+    # otherwise its bytes per element are scaled, and the line says which.
+    traffic, traffic_src = None, None
     wl_prof = "c3" if wl["name"] == "c3" else "c2"
-    profs = sorted((ROOT / "profiles").glob(f"ncu_traffic_{wl_prof}_r*.json"))
-    if profs:
+    kname = "encode_tiles" if dominant == "encode" else "decode_persistent"
+    for prof in sorted((ROOT / "profiles").glob(f"ncu_traffic_{wl_prof}_r*.json")):
         try:
-            per_elem = json.loads(profs[-1].read_text())["dram_bytes_per_element"]
-            kname = "encode_tiles" if dominant == "encode" else "decode_persistent"
-            if kname in per_elem:
-                traffic = int(per_elem[kname] * n)
-        except (ValueError, KeyError):
-            traffic = None
+            d = json.loads(prof.read_text())
+        except ValueError:
+            continue
+        if d.get("n_elements_profiled") == n and kname in d.get("dram_bytes_per_launch", {}):
+            traffic, traffic_src = int(d["dram_bytes_per_launch"][kname]), \
+                f"{prof.name}: measured at this size"
+        elif traffic_src is None or "measured" not in traffic_src:
+            if kname in d.get("dram_bytes_per_element", {}):
+                traffic = int(d["dram_bytes_per_element"][kname] * n)
+                traffic_src = (f"{prof.name}: {d['n_elements_profiled']}-element capture, "
+                               "bytes/element scaled")
 
     value = world * raw * K / (tot_ms / 1e3) / 1e9
     enc_gbs = world * raw * K / (enc_ms / 1e3) / 1e9
@@ -365,12 +402,8 @@ def run_ours(args) -> None:
         "steps": K, "warmup": args.warmup, "ms_per_step": round(tot_ms / K, 4),
         "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
         "dtype": "u16" if fmt.word_bits == 16 else "u8", "data": "synthetic",
-        "config": {"workload": wl["desc"], "elements_per_gpu": n, "chunk": args.chunk,
-                   "code_bits": 4, "escape_rate_target": args.escape_rate,
-                   "escape_rate": round(m / n, 6), "codebook": list(book.entries),
-                   "l2": "inputs (>=2 GiB/rank) exceed the 126 MB L2; no flush needed",
-                   "step": "encode (K2) + decode (K3+K4), round trip",
-                   **({"elements_override": n} if args.elements else {})},
+        "config": bench_config(wl, args, n, book.entries),
+        "escape_rate": round(m / n, 6),
         "encode_gbs": round(enc_gbs, 2), "decode_gbs": round(dec_gbs, 2),
         "per_rank_gbs": {"min": round(raw * K / (max(per_rank_ms) / 1e3) / 1e9, 2),
                          "max": round(raw * K / (min(per_rank_ms) / 1e3) / 1e9, 2),
@@ -381,6 +414,7 @@ def run_ours(args) -> None:
         "roofline": {"bound": "hbm", "kernel": dominant, "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "encode_frac": round(alg_bytes / (enc_launch_ms / 1e3) / 1e9 / peak, 4),
                      "decode_frac": round(alg_bytes / (dec_launch_ms / 1e3) / 1e9 / peak, 4)},
@@ -450,14 +484,19 @@ def cpu_baseline_leg(args, wl, book, book_w, esc, words, eng, m) -> dict:
            "escape_values": streams.escape_values[:mm].cpu().numpy()}
     ok = cpu_bench.slice_parity(w, fmt_id, book.entries, args.chunk, sec)
     assert ok, "GPU sections differ from the oracle on the verification slice"
-    workers = max(1, min(os.cpu_count() or 1, 32))
-    per = 1 << 24   # 16 procs x 2^24 = a 2^28-word sample (~10-15 CPU-s)
-    r = cpu_bench.roundtrip_throughput(fmt_id, book.entries, book_w, esc, args.escape_rate,
-                                       args.chunk, per, workers, 1, seed=args.seed)
+    with oracle_pool(wl, args, book.entries, book_w, esc) as pool:
+        one = pool.one_core()
+        r = pool.step()
+        workers = pool.workers
+    lg = CPU_WORDS_PER_PROC.bit_length() - 1
     return {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": workers, "kind": "port",
-            "sample": f"{workers} procs x 2^24 words, one encode+decode each "
+            "sample": f"{workers} procs x 2^{lg} words, one encode+decode each "
                       f"({r['cpu_seconds']:.1f} CPU-s); numpy oracle of the reference codec",
             "encode_gbs": round(r["encode_gbs"], 4), "decode_gbs": round(r["decode_gbs"], 4),
+            "one_core": {"value": round(one["gbs"], 4), "cores": 1,
+                         "encode_gbs": round(one["encode_gbs"], 4),
+                         "decode_gbs": round(one["decode_gbs"], 4),
+                         "sample": f"1 proc x 2^{lg} words, one encode + decode"},
             "slice_parity": "2^20-word prefix: GPU sections == oracle"}
 
 

@@ -44,23 +44,35 @@ def word_dtype(fmt: int):
 # ---------------------------------------------------------------- L0 bits
 def split(words: np.ndarray, fmt: int):
     """(exponent, sign|mantissa) planes — formats.py:113-133."""
-    w = np.asarray(words).astype(np.uint32)
     wb, eb, sb = FORMATS[fmt]
+    if wb == 16:
+        # byte-plane form of the same bit moves (u8 arithmetic only): for
+        # w = hi:lo, exp = hi[6:0]:lo[7], sm = hi[7]:lo[6:0]
+        b = np.ascontiguousarray(words, dtype=np.uint16).view(np.uint8)
+        lo, hi = b[0::2], b[1::2]
+        exp = (hi << np.uint8(1)) | (lo >> np.uint8(7))
+        sm = (hi & np.uint8(0x80)) | (lo & np.uint8(0x7F))
+        return exp, sm
+    w = np.asarray(words, dtype=np.uint8)
     mant_bits = sb - 1
-    sign = w >> (wb - 1)
-    exp = (w >> mant_bits) & ((1 << eb) - 1)
-    sm = (sign << mant_bits) | (w & ((1 << mant_bits) - 1))
-    return exp.astype(np.uint8), sm.astype(np.uint8)
+    exp = (w >> np.uint8(mant_bits)) & np.uint8((1 << eb) - 1)
+    sm = ((w >> np.uint8(wb - 1)) << np.uint8(mant_bits)) | (w & np.uint8((1 << mant_bits) - 1))
+    return exp, sm
 
 
 def join(exp: np.ndarray, sm: np.ndarray, fmt: int) -> np.ndarray:
     """Inverse of :func:`split` — formats.py:136-155."""
     wb, eb, sb = FORMATS[fmt]
+    e = np.asarray(exp, dtype=np.uint8)
+    a = np.asarray(sm, dtype=np.uint8)
+    if wb == 16:
+        out = np.empty(2 * e.size, dtype=np.uint8)
+        out[1::2] = (a & np.uint8(0x80)) | (e >> np.uint8(1))
+        out[0::2] = (e << np.uint8(7)) | (a & np.uint8(0x7F))
+        return out.view(np.uint16)
     mant_bits = sb - 1
-    e = np.asarray(exp).astype(np.uint32)
-    a = np.asarray(sm).astype(np.uint32)
-    w = ((a >> mant_bits) << (wb - 1)) | (e << mant_bits) | (a & ((1 << mant_bits) - 1))
-    return w.astype(word_dtype(fmt))
+    return (((a >> np.uint8(mant_bits)) << np.uint8(wb - 1)) | (e << np.uint8(mant_bits))
+            | (a & np.uint8((1 << mant_bits) - 1)))
 
 
 def packed_len(count: int, width: int) -> int:
@@ -79,28 +91,40 @@ def pack_le(symbols, width: int) -> bytes:
         return b""
     if width == 8:
         return s.tobytes()
+    if width == 4:  # element 2i in the low nibble (formats.py:180-183)
+        if s.size & 1:
+            s = np.append(s, np.uint8(0))
+        return (s[0::2] | (s[1::2] << np.uint8(4))).tobytes()
     bit_planes = (s[:, None] >> np.arange(width, dtype=np.uint8)) & 1
     return np.packbits(bit_planes.reshape(-1), bitorder="little").tobytes()
 
 
 def unpack_le(data: bytes, count: int, width: int) -> np.ndarray:
-    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    buf = np.frombuffer(data, dtype=np.uint8)
     if count == 0:
         return np.zeros(0, dtype=np.uint8)
     if width == 8:
         return buf[:count].copy()
+    if width == 4:
+        out = np.empty(2 * buf.size, dtype=np.uint8)
+        out[0::2] = buf & np.uint8(0x0F)
+        out[1::2] = buf >> np.uint8(4)
+        return out[:count]
     bits = np.unpackbits(buf, bitorder="little", count=count * width)
     weights = (1 << np.arange(width)).astype(np.uint16)
     return (bits.reshape(count, width).astype(np.uint16) @ weights).astype(np.uint8)
 
 
 def pad_bits_clear(data: bytes, count: int, width: int) -> bool:
-    """formats.py:223-231."""
+    """formats.py:223-231: every bit past count*width is zero."""
     used = count * width
-    if used == len(data) * 8:
+    buf = np.frombuffer(data, dtype=np.uint8)
+    if used >= buf.size * 8:
         return True
-    bits = np.unpackbits(np.frombuffer(bytes(data), dtype=np.uint8), bitorder="little")
-    return not bits[used:].any()
+    first = used // 8
+    if int(buf[first]) >> (used % 8):
+        return False
+    return not buf[first + 1:].any()
 
 
 # ---------------------------------------------------------- calibration
@@ -166,11 +190,13 @@ def encode(words: np.ndarray, p: Params, book) -> dict:
     n = words.size
     exp, sm = split(words, p.fmt)
     enc, _, member = tables(book, p.fmt)
-    is_member = member[exp]
     fill = ((1 << p.code_bits) - 1) if p.sentinel else DUMMY
-    codes = np.where(is_member, enc[exp], np.uint8(fill)).astype(np.uint8)
-    where = np.nonzero(~is_member)[0]
-    values = exp[where].astype(np.uint8)
+    # one gather through the encode table; non-members carry ESCAPE_MARK
+    # (codec.py:303-309: member -> code, else the escape/dummy code)
+    codes = enc[exp]
+    where = np.flatnonzero(codes == ESCAPE_MARK)
+    codes[where] = fill
+    values = exp[where]
     if p.sentinel:
         counts = np.zeros(0, dtype=np.uint32)
         pos = np.zeros(0, dtype=np.uint8)

@@ -6,6 +6,7 @@ Writes profiles/ncu_<tag>.md and profiles/ncu_traffic_<tag>.json.
 import csv
 import io
 import json
+import os
 import re
 import subprocess
 import sys
@@ -57,7 +58,7 @@ def main():
              "| kernel | time (us) | DRAM read (MB) | DRAM write (MB) | DRAM B/elem | DRAM % peak | "
              "issue % | ALU % | regs | grid x block |",
              "|---|---|---|---|---|---|---|---|---|---|"]
-    traffic = {}
+    traffic, absolute = {}, {}
     for k in kernels:
         tot = (k.get("dram_read") or 0) + (k.get("dram_write") or 0)
         lines.append(
@@ -67,11 +68,16 @@ def main():
             f"{k.get('grid', 0):.0f} x {k.get('block', 0):.0f} |")
         name = re.sub(r"^void ", "", k["kernel"]).split("<")[0].split("::")[-1]
         traffic.setdefault(name, tot / n)
-    (ROOT / "profiles").mkdir(exist_ok=True)
-    (ROOT / "profiles" / f"ncu_{tag}.md").write_text("\n".join(lines) + "\n")
-    (ROOT / "profiles" / f"ncu_traffic_{tag}.json").write_text(json.dumps(
+        absolute.setdefault(name, int(tot))
+    # SZ_PROFILES_DIR: write elsewhere (on the GPU box: gpurun_out/, which
+    # comes back; the .ncu-rep files themselves may be too large to)
+    out_dir = Path(os.environ.get("SZ_PROFILES_DIR", ROOT / "profiles"))
+    out_dir.mkdir(exist_ok=True)
+    (out_dir / f"ncu_{tag}.md").write_text("\n".join(lines) + "\n")
+    (out_dir / f"ncu_traffic_{tag}.json").write_text(json.dumps(
         {"source": Path(rep).name, "n_elements_profiled": n,
-         "dram_bytes_per_element": traffic}, indent=1) + "\n")
+         "dram_bytes_per_element": traffic, "dram_bytes_per_launch": absolute},
+        indent=1) + "\n")
     print("\n".join(lines))
 
 
