@@ -45,17 +45,23 @@ def _stale(verbose: bool) -> bool:
     return any(d.stat().st_mtime > lib_m for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> Path:
-    if not force and not _stale(verbose):
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+          variant: str | None = None, defines: tuple = ()) -> Path:
+    """``variant``/``defines``: an A/B build (extra -D flags) into
+    libsz_b200.<variant>.so beside the product library (see _native)."""
+    lib_out = LIB if variant is None else PKG / f"libsz_b200.{variant}.so"
+    if variant is None and not force and not _stale(verbose):
         return LIB
-    BUILD.mkdir(parents=True, exist_ok=True)
+    build_dir = BUILD if variant is None else BUILD.parent / f"csrc_{variant}"
+    build_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_v else []
     # e.g. SZ_NVCC_DEFINES="SZ_TIMERS" for the per-role pipeline timers
     extra += [f"-D{d}" for d in os.environ.get("SZ_NVCC_DEFINES", "").split() if d]
+    extra += [f"-D{d}" for d in defines]
 
     def compile_one(src: Path) -> tuple[Path, str]:
-        obj = BUILD / (src.stem + ".o")
+        obj = build_dir / (src.stem + ".o")
         cmd = [cc, *ARCH, *FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
@@ -68,13 +74,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         for _, log in results:
             if log.strip():
                 print(log, file=sys.stderr)
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib_out.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *[str(o) for o, _ in results], "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

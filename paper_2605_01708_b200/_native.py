@@ -10,6 +10,7 @@ nothing torch-typed crosses the ABI (plain pointers, sizes, a stream handle).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
@@ -18,6 +19,10 @@ import torch
 from .errors import ConfigError, NativeError
 
 LIB_PATH = Path(__file__).resolve().parent / "libsz_b200.so"
+# A/B experiments only (scripts/ab_variants.sh): load a variant build of the
+# same library from another in-tree path
+if os.environ.get("SZ_LIB_VARIANT"):
+    LIB_PATH = Path(__file__).resolve().parent / f"libsz_b200.{os.environ['SZ_LIB_VARIANT']}.so"
 ABI_VERSION = 1
 
 SZ_OK, SZ_ECONFIG, SZ_EWORKSPACE, SZ_EALIGN, SZ_ECUDA, SZ_EOUTPUT = range(6)

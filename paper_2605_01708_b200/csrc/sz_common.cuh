@@ -9,6 +9,8 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 #include <cuda_runtime.h>
 
 #include "../../include/splitzip_b200.h"
@@ -22,6 +24,58 @@
 #endif
 
 namespace sz {
+
+// ---------------------------------------------------------------- launch setup
+// Per (kernel, device): raise the dynamic shared-memory limit once and cache
+// the occupancy and SM count, so a launch costs no attribute calls (a 64 MiB
+// handoff piece encodes in ~18 us of device time; per-call
+// cudaFuncSetAttribute + occupancy queries were a visible share of it).
+// SM count of the current device, cached per device ordinal.
+inline int device_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = sms;
+  }
+  return cached[dev];
+}
+
+struct KernelSetup {
+  cudaError_t err;
+  int per_sm;  // resident CTAs per SM at (threads, smem)
+  int sms;
+};
+inline KernelSetup kernel_setup(const void* kern, int smem, int threads) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, KernelSetup> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (reinterpret_cast<uint64_t>(kern) << 8) ^ static_cast<uint64_t>(dev) ^
+                       (static_cast<uint64_t>(smem) << 48) ^ (static_cast<uint64_t>(threads) << 40);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  KernelSetup k{cudaSuccess, 1, 148};
+  if (smem > 0)
+    k.err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (k.err == cudaSuccess) {
+    int per_sm = 0;
+    k.err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    k.per_sm = per_sm;
+  }
+  cudaDeviceGetAttribute(&k.sms, cudaDevAttrMultiProcessorCount, dev);
+  if (k.err == cudaSuccess) {
+    std::lock_guard<std::mutex> g(mu);
+    cache.emplace(key, k);
+  }
+  return k;
+}
 
 constexpr int kThreads = 256;          // CTA size of every streaming kernel
 constexpr int kWarps = kThreads / 32;

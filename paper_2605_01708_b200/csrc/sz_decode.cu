@@ -949,26 +949,18 @@ DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
   return w;
 }
 
-int sm_count() {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
-}
 
 // Explicit modes: persistent warp-specialised kernel.
 template <int FMT, int CB, int POSB>
 cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
   auto kern = decode_persistent<FMT, CB, POSB>;
   const int smem = static_cast<int>(sizeof(DecSmem<FMT>));
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDecThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const uint64_t want = static_cast<uint64_t>(sm_count()) * per_sm;
+  const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kDecThreads);
+  if (ks.err != cudaSuccess) return ks.err;
+  const int per_sm = ks.per_sm < 1 ? 1 : ks.per_sm;
+  const uint64_t want = static_cast<uint64_t>(ks.sms) * per_sm;
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
-  e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, s, p, a);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kDecThreads), smem, s, p, a);
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
 template <int FMT, int CB>
@@ -1052,7 +1044,7 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
   if (p->abs32) {
-    const unsigned g = static_cast<unsigned>(sm_count() * 8);
+    const unsigned g = static_cast<unsigned>(device_sms() * 8);
     abs_bounds_kernel<<<g, kThreads, 0, s>>>(static_cast<const uint32_t*>(in->d_positions),
                                              in->d_n_escapes, m, n, decode_tile_for(p->fmt),
                                              dtiles, w.offsets);

@@ -48,13 +48,32 @@ constexpr int kEncSlots = kEncItems * kEncDense;         // 1024 slots per tile
 constexpr int kEncTileBytes = kEncSlots * 32;           // 32 KiB of input words
 constexpr int kEncInStages = 4;
 constexpr int kEncScanSlots = 8;
-constexpr int kEscCap = 1024;                           // escape records per tile slot
-// 16 + 1 + 3 = 20 warps: a multiple of 4 so the register file splits evenly
-// (96 registers per thread at one CTA per SM).
-constexpr int kWriterWarps = 3;
-constexpr int kEncThreads = kEncDense + 32 * (1 + kWriterWarps);
+// Escape records per tile the dense warps can stage in shared memory (12.5%
+// of a BF16 tile, 6.25% of an FP8 tile); a tile past it is re-derived by K2c.
+// BF16 (7 writer warps) 1984; FP8 (3 writer warps, twice the elements per
+// tile) 2400 — what the shared memory left by the rest of EncSmem holds.
+#ifndef SZ_FP8_ESC_CAP
+#define SZ_FP8_ESC_CAP 2400
+#endif
+template <int FMT>
+constexpr int kEscValCap = FMT == SZ_BF16 ? 1984 : SZ_FP8_ESC_CAP;
+// Scratch records per tile in global memory: 1/8 of the tile's elements
+// (2048 BF16 / 4096 FP8 — a top-8 3-bit book's ~7% escapes fit), so the
+// scratch is n/8 records; tiles with more escapes go to K2c.
+template <int FMT>
+constexpr uint32_t kTileCap = kEncSlots * kEpv<FMT> / 8 < kEscValCap<FMT>
+                                  ? kEncSlots * kEpv<FMT> / 8 : kEscValCap<FMT>;
+// Writer warps: the escape records' placement is a per-tile serial chain
+// per writer, so escape-dense BF16 tiles want many (7: 16 + 1 + 7 = 24 warps
+// at 80 registers); the FP8 dense warps are issue-bound and need the
+// registers (3: 20 warps at 96).  Warp counts stay multiples of 4 so the
+// register file splits evenly.
+template <int FMT>
+constexpr int kWriterWarps = FMT == SZ_BF16 ? 7 : 3;
+template <int FMT>
+constexpr int kEncThreads = kEncDense + 32 * (1 + kWriterWarps<FMT>);
 constexpr int kProducerWarp = kEncDenseWarps;           // warp 16
-constexpr int kWriterWarp0 = kEncDenseWarps + 1;        // warps 17..19
+constexpr int kWriterWarp0 = kEncDenseWarps + 1;        // warps 17..
 
 struct EncodeArgs {
   const uint8_t* words;
@@ -71,8 +90,8 @@ struct EncodeArgs {
   int32_t counts_mode;   // 0 none, 1 direct from the scan, 2 atomics (pre-zeroed)
   unsigned long long* tile_counter;
   uint32_t* tile_esc;    // per-tile escape count
-  uint8_t* scr_pos;      // kEscCap positions per tile (POSB bytes each)
-  uint8_t* scr_val;      // kEscCap raw exponents per tile
+  uint8_t* scr_pos;      // kTileCap positions per tile (POSB bytes each)
+  uint8_t* scr_val;      // kTileCap raw exponents per tile
   const uint64_t* escape_base;  // append mode: global ordinal offset (or null)
   uint64_t* base_snapshot;      // workspace copy of *escape_base for K2b
   unsigned long long* dbg;  // optional per-role cycle counters (SZ_DEBUG_TIMERS)
@@ -92,16 +111,19 @@ struct EncodeArgs {
   int32_t seg_tmap;
 };
 
+template <int FMT>
 struct EncSmem {
   // 1024-aligned: the 128B-swizzle pattern of tensor TMA is a function of
   // shared-address bits 7-9
   alignas(1024) uint8_t in[kEncInStages][kEncTileBytes];
   uint32_t fmask[kEncScanSlots][kEncSlots];  // at fsw(slot)
-  // escape records (tile-local element index | raw exponent << 16), in
-  // arbitrary order; the writer warp derives each one's rank from fmask
-  uint32_t esc_rec[kEncScanSlots][kEscCap];
+  // the tile's escape records, (tile-local element index, raw exponent), in
+  // arbitrary order (one shared atomic per slot with escapes); the writer
+  // derives each one's rank from fmask
+  uint16_t esc_idx[kEncScanSlots][kEscValCap<FMT>];
+  uint8_t esc_val[kEncScanSlots][kEscValCap<FMT>];
   uint32_t esc_n[kEncScanSlots];
-  uint32_t slot_pref[kWriterWarps][kEncSlots];  // per-slot exclusive escape prefix, at fsw(slot)
+  uint16_t slot_pref[kWriterWarps<FMT>][kEncSlots];  // per-slot exclusive escape prefix, at fsw(slot)
   uint64_t meta[kEncScanSlots];      // tile id (~0 = end of work)
   uint64_t full[kEncInStages];       // producer -> dense (TMA bytes)
   uint64_t in_empty[kEncInStages];   // dense -> producer
@@ -341,7 +363,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 template <int FMT, int CB, int POSB>
-__global__ void __launch_bounds__(kEncThreads, 1)
+__global__ void __launch_bounds__(kEncThreads<FMT>, 1)
     encode_tiles(const __grid_constant__ sz_params p, const EncodeArgs a,
                  const __grid_constant__ CUtensorMap tmap) {
   constexpr int EPV = kEpv<FMT>;
@@ -350,9 +372,11 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   constexpr int SMB = Fmt<FMT>::kSmBits;
   constexpr int CBYTES = EPV * CB / 8;
   constexpr int SBYTES = EPV * SMB / 8;
-  constexpr int PB = POSB == 0 ? 1 : POSB;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  EncSmem& S = *reinterpret_cast<EncSmem*>(
+  constexpr int NW = kWriterWarps<FMT>;
+  constexpr int NT = kEncThreads<FMT>;
+  constexpr int VCAP = kEscValCap<FMT>;
+  EncSmem<FMT>& S = *reinterpret_cast<EncSmem<FMT>*>(
       smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -361,7 +385,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
   constexpr int TE = kT4Entries<FMT>;
   __shared__ __align__(1024) uint32_t s_tab[4 * TE];
   const uint8_t* s_lut = reinterpret_cast<const uint8_t*>(s_tab);
-  for (int i = tid; i < 4 * TE; i += kEncThreads) {
+  for (int i = tid; i < 4 * TE; i += NT) {
     const int k = i / TE, e = i % TE;
     if constexpr (FMT == SZ_E5M2 && kE5FullByte) {  // e is the whole byte here
       const uint32_t m = p.enc_lut[(e >> 2) & 31];
@@ -420,10 +444,10 @@ __global__ void __launch_bounds__(kEncThreads, 1)
           tile = atomicAdd(a.tile_counter, 1ull);
         }
         if (tile >= a.num_tiles) {
-          // end markers in this slot and the next kWriterWarps-1 (one per
+          // end markers in this slot and the next NW-1 (one per
           // writer residue class); the dense warps relay them (computed)
           S.meta[q] = ~0ull;
-          for (uint32_t k = 1; k < kWriterWarps; ++k) {
+          for (uint32_t k = 1; k < NW; ++k) {
             const uint32_t qk = (it + k) % kEncScanSlots, pk = ((it + k) / kEncScanSlots) & 1;
             mbar_wait(&S.scan_empty[qk], pk ^ 1);
             S.meta[qk] = ~0ull;
@@ -498,7 +522,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       t_wait += c1 - c0;
       const uint64_t tile = S.meta[q];
       if (tile == ~0ull) {
-        for (uint32_t k = 0; k < kWriterWarps; ++k)
+        for (uint32_t k = 0; k < NW; ++k)
           mbar_arrive(&S.computed[(it + k) % kEncScanSlots]);
         break;
       }
@@ -508,6 +532,11 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       uint8_t* const stile = a.sm + tile_e0 * SMB / 8;
       uint32_t x[kEncItems][8];
       int nv[kEncItems];
+      // (steady state) byte offsets of the slot's two 16-byte halves in its
+      // 128-byte stage row; the escape loop below re-reads words from there
+      const uint32_t rsw = (tid >> 2) & 7, cc0 = 2 * (tid & 3);
+      const uint32_t off0 = a.use_tmap ? ((cc0 ^ rsw) << 4) : (tid & 3) * 32;
+      const uint32_t off1 = a.use_tmap ? (((cc0 + 1) ^ rsw) << 4) : (tid & 3) * 32 + 16;
       if (!tail_tile) {
         // steady state: every slot is full and in the TMA stage.  Slot
         // i*512 + tid is row (slot >> 2) of 128 B, 16-byte chunks 2(tid&3) and
@@ -515,9 +544,6 @@ __global__ void __launch_bounds__(kEncThreads, 1)
         // row & 7 = (tid >> 2) & 7 — per-thread constants.  A quarter-warp then
         // reads 8 distinct chunks of 2 rows: no bank conflicts (the linear
         // layout's 32-byte stride made every read 2-way conflicted).
-        const uint32_t rsw = (tid >> 2) & 7, c0 = 2 * (tid & 3);
-        const uint32_t off0 = a.use_tmap ? ((c0 ^ rsw) << 4) : (tid & 3) * 32;
-        const uint32_t off1 = a.use_tmap ? (((c0 + 1) ^ rsw) << 4) : (tid & 3) * 32 + 16;
 #pragma unroll
         for (int i = 0; i < kEncItems; ++i) {
           const uint8_t* row = S.in[s] + (i * kEncDense + tid) / 4 * 128;
@@ -543,7 +569,7 @@ __global__ void __launch_bounds__(kEncThreads, 1)
           }
         }
       }
-      mbar_arrive(&S.in_empty[s]);  // input stage free: the producer may refill it
+      uint32_t fms[kEncItems];
 #pragma unroll
       for (int i = 0; i < kEncItems; ++i) {
         const int slot = i * kEncDense + tid;
@@ -557,22 +583,43 @@ __global__ void __launch_bounds__(kEncThreads, 1)
                                           tile_e0 + static_cast<uint64_t>(slot) * EPV);
         }
         S.fmask[q][fsw(slot)] = fm;
-        if (fm) {  // rare: append (element, raw exponent) records for the writer
-          uint32_t r = atomicAdd(&S.esc_n[q], static_cast<uint32_t>(__popc(fm)));
-          // a tile past kEscCap records is re-derived whole by K2c: no record
-          // of it is used, so stop writing them
-          uint32_t f = r + __popc(fm) <= kEscCap ? fm : 0u;
-          while (f) {  // compact loop; x[] read through selects (no local memory)
+        fms[i] = fm;
+      }
+      // input stage free: the producer may refill it (a thread with escapes
+      // holds it through its escape loop, which re-reads the words there)
+      const bool any_esc = (fms[0] | fms[1]) != 0u;
+      static_assert(kEncItems == 2, "any_esc covers two items");
+      if (!any_esc) mbar_arrive(&S.in_empty[s]);
+#pragma unroll
+      for (int i = 0; i < kEncItems; ++i) {
+        const int slot = i * kEncDense + tid;
+        const uint32_t fm = fms[i];
+        if (fm) {  // append this slot's escape records for the writer
+          const uint32_t c = static_cast<uint32_t>(__popc(fm));
+          uint32_t r = atomicAdd(&S.esc_n[q], c);
+          // a tile past VCAP is re-derived whole by K2c: none of its
+          // records is used, so stop writing them
+          uint32_t f = r + c <= VCAP ? fm : 0u;
+          const uint8_t* row = S.in[s] + (i * kEncDense + tid) / 4 * 128;
+          while (f) {  // compact loop
             const int j = __ffs(f) - 1;
             f &= f - 1;
             uint32_t word;
-            if constexpr (WB == 2) word = (pick<8>(x[i], j >> 1) >> (16 * (j & 1))) & 0xFFFFu;
-            else word = (pick<8>(x[i], j >> 2) >> (8 * (j & 3))) & 0xFFu;
-            S.esc_rec[q][r++] = static_cast<uint32_t>(slot * EPV + j) |
-                                (raw_exponent<FMT>(word) << 16);
+            if (!tail_tile) {  // the word again from the (still held) input stage
+              const uint32_t bo = static_cast<uint32_t>(j) * WB;
+              const uint8_t* wp = row + ((bo >> 4) ? off1 : off0) + (bo & 15u);
+              if constexpr (WB == 2) word = *reinterpret_cast<const uint16_t*>(wp);
+              else word = *wp;
+            } else {  // x[] read through selects (no local memory)
+              if constexpr (WB == 2) word = (pick<8>(x[i], j >> 1) >> (16 * (j & 1))) & 0xFFFFu;
+              else word = (pick<8>(x[i], j >> 2) >> (8 * (j & 3))) & 0xFFu;
+            }
+            S.esc_idx[q][r] = static_cast<uint16_t>(slot * EPV + j);
+            S.esc_val[q][r++] = static_cast<uint8_t>(raw_exponent<FMT>(word));
           }
         }
       }
+      if (any_esc) mbar_arrive(&S.in_empty[s]);
       mbar_arrive(&S.computed[q]);
       t_work += SZ_CLOCK() - c1;
     }
@@ -585,11 +632,11 @@ __global__ void __launch_bounds__(kEncThreads, 1)
 
   // ---------------------------------------------------------------- writer warps
   constexpr int SPL = kEncSlots / 32;  // 32 consecutive slots per lane
-  const int ww = warp - kWriterWarp0;  // owns iterations it == ww (mod kWriterWarps)
-  uint32_t* sp = S.slot_pref[ww];
+  const int ww = warp - kWriterWarp0;  // owns iterations it == ww (mod NW)
+  uint16_t* sp = S.slot_pref[ww];
   const uint32_t key = fsw_key(lane);  // this lane's slots: lane*SPL + (j ^ key)
   long long t_wait = 0, t_work = 0;
-  for (uint32_t it = ww;; it += kWriterWarps) {
+  for (uint32_t it = ww;; it += NW) {
     const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
     const long long c0 = SZ_CLOCK();
     mbar_wait(&S.computed[q], qph);
@@ -655,26 +702,45 @@ __global__ void __launch_bounds__(kEncThreads, 1)
       }
     }
 
-    // tile-local escape records, ascending element order, into the scratch slot
-    const uint32_t n_rec = S.esc_n[q];
-    if (total && total <= kEscCap && n_rec == total) {
+    // The tile's escape records into its scratch slot in ascending element
+    // order: per-slot prefixes from the lane scan, then consecutive lanes on
+    // consecutive records (balanced whatever the escapes' clustering), each
+    // record's rank = its slot's prefix + the escapes below it in the slot.
+    if (total && total <= VCAP) {
       uint32_t run = excl_lane;
       for (int j = 0; j < SPL; ++j) {
         sp[lane * SPL + (j ^ key)] = run;
         run += __popc(fm[j ^ key]);
       }
       __syncwarp();
-      uint8_t* spos = a.scr_pos + tile * kEscCap * PB;
-      uint8_t* sval = a.scr_val + tile * kEscCap;
-      for (uint32_t r = lane; r < n_rec; r += 32) {
-        const uint32_t rec = S.esc_rec[q][r];
-        const uint32_t local = rec & 0xFFFFu, slot = local / EPV, b = local % EPV;
-        const uint32_t rank = sp[fsw(slot)] + __popc(S.fmask[q][fsw(slot)] & ((1u << b) - 1u));
-        sval[rank] = static_cast<uint8_t>(rec >> 16);
-        put_position<POSB>(spos, rank, tile_e0 + local, a.chunk, a.chunk_shift);
+      uint8_t* const sval = a.scr_val + tile * kTileCap<FMT>;
+      uint8_t* const spos = a.scr_pos + tile * kTileCap<FMT> * (POSB ? POSB : 1);
+      // positions in 32-bit arithmetic: chunk-relative = (tile start mod
+      // chunk + local) mod chunk; abs32 = tile start + local (n < 2^32)
+      const uint32_t pbase = POSB == 4 ? static_cast<uint32_t>(tile_e0)
+                             : static_cast<uint32_t>(a.chunk_shift >= 0
+                                                         ? tile_e0 & (a.chunk - 1)
+                                                         : tile_e0 % a.chunk);
+      const uint32_t* const fmq = S.fmask[q];
+      const uint16_t* const idq = S.esc_idx[q];
+      const uint8_t* const vaq = S.esc_val[q];
+#pragma unroll 4
+      for (uint32_t r = lane; r < total; r += 32) {
+        const uint32_t local = idq[r];
+        const uint32_t slot = local / EPV, b = local % EPV;
+        const uint32_t fs = fsw(slot);
+        const uint32_t rank = sp[fs] + __popc(fmq[fs] & ((1u << b) - 1u));
+        sval[rank] = vaq[r];
+        if constexpr (POSB == 4) {
+          reinterpret_cast<uint32_t*>(spos)[rank] = pbase + local;
+        } else if constexpr (POSB == 1 || POSB == 2) {
+          uint32_t pos = pbase + local;
+          pos = a.chunk_shift >= 0 ? (pos & (a.chunk - 1)) : (pos % a.chunk);
+          if constexpr (POSB == 2) reinterpret_cast<uint16_t*>(spos)[rank] = static_cast<uint16_t>(pos);
+          else spos[rank] = static_cast<uint8_t>(pos);
+        }
       }
     }
-    // (tiles with more than kEscCap escapes are re-derived by escape_gather)
     __syncwarp();
     if (lane == 0) S.esc_n[q] = 0;
     __syncwarp();
@@ -751,6 +817,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t base = *a.base_snapshot;
     // each lane owns kTilesPerLane consecutive tiles of the group
     constexpr int kTilesPerLane = kGatherTiles / 32;
+    constexpr uint32_t CAP = kTileCap<FMT>;
     uint32_t c[kTilesPerLane];
     uint64_t lsum = 0;
     uint32_t rsum = 0;
@@ -759,7 +826,7 @@ __global__ void __launch_bounds__(kThreads)
       const uint64_t t = t0 + lane * kTilesPerLane + j;
       c[j] = t < a.num_tiles ? a.tile_esc[t] : 0u;
       lsum += c[j];
-      rsum += c[j] <= kEscCap ? c[j] : 0u;
+      rsum += c[j] <= CAP ? c[j] : 0u;
     }
     uint64_t incl = lsum;
     uint32_t rincl = rsum;
@@ -774,7 +841,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int j = 0; j < kTilesPerLane; ++j) {
         rpref[lane * kTilesPerLane + j] = rrun;
-        rrun += c[j] <= kEscCap ? c[j] : 0u;
+        rrun += c[j] <= CAP ? c[j] : 0u;
       }
       if (lane == 31) rpref[kGatherTiles] = rincl;
     }
@@ -821,8 +888,8 @@ __global__ void __launch_bounds__(kThreads)
       for (int u = 0; u < TU; ++u) {
         const int k = k0 + u;
         cnt[u] = k < k_hi ? tcnt[k] : 0u;   // 0 past the last tile of the stream
-        if (cnt[u] > kEscCap) cnt[u] = 0;     // heavy: K2c's
-        src[u] = (t0 + k) * kEscCap + lane;
+        if (cnt[u] > kTileCap<FMT>) cnt[u] = 0;  // heavy: K2c's
+        src[u] = (t0 + k) * kTileCap<FMT> + lane;
         dst[u] = (k < k_hi ? tpref[k] : 0) + lane;
         live[u] = lane < cnt[u] && dst[u] < a.capacity;
       }
@@ -870,7 +937,7 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t in_tile = r - rpref[lo];
         dst[u] = tpref[lo] + in_tile;
         live[u] = r0 + u * kThreads < g_total && dst[u] < a.capacity;
-        src[u] = (t0 + lo) * kEscCap + in_tile;
+        src[u] = (t0 + lo) * kTileCap<FMT> + in_tile;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -896,7 +963,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int j = 0; j < kGatherTiles / 32; ++j) {
       const int k = j * 32 + lane;
       const uint64_t tile = t0 + k;
-      if (tile < a.num_tiles && tcnt[k] > kEscCap) {
+      if (tile < a.num_tiles && tcnt[k] > kTileCap<FMT>) {
         const unsigned int slot = atomicAdd(a.heavy_count, 1u);
         a.heavy_list[slot] = static_cast<uint32_t>(tile);
         a.heavy_pref[slot] = tpref[k];
@@ -1131,6 +1198,9 @@ using namespace sz;
 uint64_t encode_tile_for(uint32_t fmt) {
   return static_cast<uint64_t>(kEncSlots) * (fmt == SZ_BF16 ? 16 : 32);
 }
+uint64_t tile_cap_for(uint32_t fmt) {
+  return fmt == SZ_BF16 ? kTileCap<SZ_BF16> : (fmt == SZ_E5M2 ? kTileCap<SZ_E5M2> : kTileCap<SZ_E4M3>);
+}
 int pos_bytes(const sz_params* p) {
   return p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
 }
@@ -1160,7 +1230,6 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 EncWs carve(void* base, uint64_t n, const sz_params* p) {
   EncWs w{};
   const uint64_t tiles = (n + encode_tile_for(p->fmt) - 1) / encode_tile_for(p->fmt);
-  const uint64_t groups = (tiles + kGatherTiles - 1) / kGatherTiles;
   const int pb = pos_bytes(p) ? pos_bytes(p) : 1;
   uint8_t* b = static_cast<uint8_t*>(base);
   size_t off = 0;
@@ -1174,10 +1243,11 @@ EncWs carve(void* base, uint64_t n, const sz_params* p) {
   w.zero_bytes = off;
   w.tile_esc = reinterpret_cast<uint32_t*>(b + off);
   off = align256(off + tiles * sizeof(uint32_t));
+  const uint64_t cap = tile_cap_for(p->fmt);
   w.scr_pos = b + off;
-  off = align256(off + tiles * kEscCap * pb);
+  off = align256(off + tiles * cap * pb);
   w.scr_val = b + off;
-  off = align256(off + tiles * kEscCap);
+  off = align256(off + tiles * cap);
   w.heavy_list = reinterpret_cast<uint32_t*>(b + off);
   off = align256(off + tiles * sizeof(uint32_t));
   w.heavy_pref = reinterpret_cast<uint64_t*>(b + off);
@@ -1188,23 +1258,18 @@ EncWs carve(void* base, uint64_t n, const sz_params* p) {
   return w;
 }
 
-int sm_count() {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;
-}
 
 template <int FMT, int CB, int POSB>
 cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
                           const CUtensorMap& tm, cudaStream_t s) {
   auto kern = encode_tiles<FMT, CB, POSB>;
-  const int smem = static_cast<int>(sizeof(EncSmem)) + 1024;  // + alignment slack
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  const uint64_t want = static_cast<uint64_t>(sm_count());
+  const int smem = static_cast<int>(sizeof(EncSmem<FMT>)) + 1024;  // + alignment slack
+  const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kEncThreads<FMT>);
+  if (ks.err != cudaSuccess) return ks.err;
+  cudaError_t e;
+  const uint64_t want = static_cast<uint64_t>(ks.sms);
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
-  e = launch_pdl(kern, dim3(grid), dim3(kEncThreads), smem, s, p, a, tm);
+  e = launch_pdl(kern, dim3(grid), dim3(kEncThreads<FMT>), smem, s, p, a, tm);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   {
@@ -1224,15 +1289,9 @@ cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherA
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // one wave of K2c CTAs (as many as fit per SM next to nothing else)
-  static const int heavy_per_sm = [] {
-    int blocks = 0;
-    if (cudaFuncSetAttribute(escape_heavy<FMT, POSB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kHeavySmem<FMT>) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, escape_heavy<FMT, POSB>, kThreads,
-                                                      kHeavySmem<FMT>) != cudaSuccess)
-      return 0;
-    return blocks;
-  }();
+  const KernelSetup hs = kernel_setup(reinterpret_cast<const void*>(escape_heavy<FMT, POSB>),
+                                      kHeavySmem<FMT>, kThreads);
+  const int heavy_per_sm = hs.err == cudaSuccess ? hs.per_sm : 0;
   if (heavy_per_sm <= 0) return cudaErrorInvalidConfiguration;
   const uint64_t heavy_grid = want * static_cast<uint64_t>(heavy_per_sm);
   return launch_pdl(escape_heavy<FMT, POSB>,

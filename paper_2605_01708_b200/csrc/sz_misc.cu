@@ -9,32 +9,35 @@
 namespace sz {
 
 // ------------------------------------------------------------------ K1
-// build_histogram (calibration.py:79-85).  Privatised shared-memory bins:
-// every warp owns HIST_COLS copies of the histogram and lane l increments
-// copy (l % HIST_COLS), so the skewed KV exponent distribution (one bin holds
-// ~28% of elements) costs at most 32/HIST_COLS-way same-address serialisation
-// per warp instruction instead of 9-10-way.  Bins are merged per CTA and added
-// to the (pre-zeroed) global u64 counts.
+// build_histogram (calibration.py:79-85).  Privatised shared-memory bins,
+// [copy][bin][lane]: lane l increments column l of its copy, so the 32
+// atomics of a warp instruction hit 32 distinct words in 32 distinct banks —
+// one pass, whatever the (skewed: one bin holds ~28% of KV exponents)
+// distribution.  BF16 shares one 256 x 32 copy (32 KiB) per CTA among its
+// warps (several CTAs per SM); FP8 keeps a copy per warp (4 KiB / 2 KiB).
+// Bins are merged per CTA and added to the (pre-zeroed) global u64 counts.
 template <int FMT>
 struct HistCfg {
   static constexpr int kBins = 1 << Fmt<FMT>::kExpBits;
-  static constexpr int kCols = FMT == SZ_BF16 ? 8 : 32;
-  static constexpr int kSmemWords = kWarps * kBins * kCols;
+  static constexpr int kCols = 32;
+  static constexpr int kCopies = FMT == SZ_BF16 ? 1 : kWarps;
+  static constexpr int kSmemWords = kCopies * kBins * kCols;
 };
 
 template <int FMT>
-__device__ __forceinline__ void hist_vec(uint32_t* h, const uint32_t (&x)[8], int col) {
+__device__ __forceinline__ void hist_vec(uint32_t* h, const uint32_t (&x)[8]) {
   constexpr int kCols = HistCfg<FMT>::kCols;
+  // h already points at column `lane` of this warp's copy
 #pragma unroll
   for (int w = 0; w < 8; ++w) {
     if constexpr (FMT == SZ_BF16) {
-      atomicAdd(&h[((x[w] >> 7) & 0xFF) * kCols + col], 1u);
-      atomicAdd(&h[((x[w] >> 23) & 0xFF) * kCols + col], 1u);
+      atomicAdd(&h[((x[w] >> 7) & 0xFF) * kCols], 1u);
+      atomicAdd(&h[((x[w] >> 23) & 0xFF) * kCols], 1u);
     } else {
       constexpr int sh = FMT == SZ_E5M2 ? 2 : 3;
       constexpr uint32_t mk = FMT == SZ_E5M2 ? 0x1F : 0x0F;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) atomicAdd(&h[((x[w] >> (8 * b + sh)) & mk) * kCols + col], 1u);
+      for (int b = 0; b < 4; ++b) atomicAdd(&h[((x[w] >> (8 * b + sh)) & mk) * kCols], 1u);
     }
   }
 }
@@ -51,8 +54,7 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint8_t* __restric
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < C::kSmemWords; i += kThreads) hsm[i] = 0;
   __syncthreads();
-  uint32_t* h = hsm + warp * C::kBins * C::kCols;
-  const int col = lane % C::kCols;
+  uint32_t* h = hsm + (warp % C::kCopies) * C::kBins * C::kCols + lane;
   const uint64_t nvec = n / EPV;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
   uint64_t v = static_cast<uint64_t>(blockIdx.x) * kThreads + tid;
@@ -61,25 +63,26 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint8_t* __restric
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) ld_stream256(words + (v + u * stride) * 32, x[u]);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) hist_vec<FMT>(h, x[u], col);
+    for (int u = 0; u < UNROLL; ++u) hist_vec<FMT>(h, x[u]);
   }
   for (; v < nvec; v += stride) {
     uint32_t x[8];
     ld_stream256(words + v * 32, x);
-    hist_vec<FMT>(h, x, col);
+    hist_vec<FMT>(h, x);
   }
   if (blockIdx.x == 0) {  // ragged tail (< EPV elements)
     for (uint64_t i = nvec * EPV + tid; i < n; i += kThreads) {
       uint32_t w = WB == 2 ? reinterpret_cast<const uint16_t*>(words)[i] : words[i];
       uint32_t e = FMT == SZ_BF16 ? (w >> 7) & 0xFF : (FMT == SZ_E5M2 ? (w >> 2) & 0x1F : (w >> 3) & 0xF);
-      atomicAdd(&h[e * C::kCols + col], 1u);
+      atomicAdd(&h[e * C::kCols], 1u);
     }
   }
   __syncthreads();
   for (int b = tid; b < C::kBins; b += kThreads) {
     unsigned long long sum = 0;
-    for (int w = 0; w < kWarps; ++w)
-      for (int c = 0; c < C::kCols; ++c) sum += hsm[(w * C::kBins + b) * C::kCols + c];
+    for (int w = 0; w < C::kCopies; ++w)
+      for (int c = 0; c < C::kCols; ++c)  // (rotated start: no bank conflicts)
+        sum += hsm[(w * C::kBins + b) * C::kCols + ((c + b) & (C::kCols - 1))];
     if (sum) atomicAdd(&counts[b], sum);
   }
 }
@@ -403,14 +406,10 @@ int sz_histogram(const void* d_words, uint64_t n, uint32_t fmt, uint64_t* d_coun
   if (!n) return SZ_OK;
   auto launch = [&](auto kern, int smem_words, uint64_t epv) {
     const size_t smem = static_cast<size_t>(smem_words) * 4;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern),
+                                        static_cast<int>(smem), kThreads);
     uint64_t want = (n / epv + kThreads - 1) / kThreads;
-    uint64_t cap = static_cast<uint64_t>(sms) * (per_sm > 0 ? per_sm : 1);
+    uint64_t cap = static_cast<uint64_t>(ks.sms) * (ks.per_sm > 0 ? ks.per_sm : 1);
     unsigned grid = static_cast<unsigned>(want < 1 ? 1 : (want < cap ? want : cap));
     kern<<<grid, kThreads, smem, s>>>(static_cast<const uint8_t*>(d_words), n,
                                       reinterpret_cast<unsigned long long*>(d_counts));

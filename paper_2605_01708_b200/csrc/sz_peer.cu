@@ -74,10 +74,17 @@ int sz_peer_wait(const uint64_t* d_flag, uint64_t value, uint64_t timeout_ns,
   // a codec kernel on another stream of this GPU (the persistent encoder
   // wants ~200 KB per SM) has to fit beside it, or that CTA would wait for
   // the poller — which may be waiting for that very kernel.
-  static const cudaError_t carve = cudaFuncSetAttribute(
-      sz::peer_wait_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-      static_cast<int>(cudaSharedmemCarveoutMaxShared));
-  if (carve != cudaSuccess) return sz_record_cuda(carve);
+  // (a function attribute of the current device's context: set once per device)
+  static bool carved[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !carved[dev]) {
+    const cudaError_t carve = cudaFuncSetAttribute(
+        sz::peer_wait_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+        static_cast<int>(cudaSharedmemCarveoutMaxShared));
+    if (carve != cudaSuccess) return sz_record_cuda(carve);
+    if (dev >= 0 && dev < 64) carved[dev] = true;
+  }
   sz::peer_wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
       d_flag, value, timeout_ns ? timeout_ns : 30000000000ull, d_timed_out);
   const cudaError_t e = cudaGetLastError();
