@@ -921,6 +921,19 @@ __global__ void __launch_bounds__(kThreads)
     // kGatherUnroll records per thread per round: all loads are issued before
     // any store, so the round costs one memory latency, not kGatherUnroll.
     constexpr int U = kGatherUnroll;
+    // r's tile = the last k with rpref[k] <= r.  A thread's records only
+    // increase (by 256 per step), so after one binary search a cursor that
+    // advances over the few tile starts in between finds each one.
+    int cur = 0;
+    {
+      const uint32_t r = static_cast<uint32_t>(g_lo + tid);
+      int hi = kGatherTiles;
+#pragma unroll
+      for (int step = 0; step < 8; ++step) {  // log2(kGatherTiles) halvings
+        const int mid = (cur + hi) >> 1;
+        if (rpref[mid] <= r) cur = mid; else hi = mid;
+      }
+    }
     for (uint64_t r0 = tid; r0 < g_total; r0 += kThreads * U) {
       uint64_t src[U], dst[U];
       uint32_t val[U], pos[U];
@@ -928,12 +941,8 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint32_t r = static_cast<uint32_t>(g_lo + r0 + u * kThreads);
-        int lo = 0, hi = kGatherTiles;  // last k with rpref[k] <= r: r's tile
-#pragma unroll
-        for (int step = 0; step < 8; ++step) {  // log2(kGatherTiles) halvings
-          const int mid = (lo + hi) >> 1;
-          if (rpref[mid] <= r) lo = mid; else hi = mid;
-        }
+        while (cur + 1 < kGatherTiles && rpref[cur + 1] <= r) ++cur;
+        const int lo = cur;
         const uint32_t in_tile = r - rpref[lo];
         dst[u] = tpref[lo] + in_tile;
         live[u] = r0 + u * kThreads < g_total && dst[u] < a.capacity;
@@ -1434,9 +1443,13 @@ int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shi
   g.base_snapshot = w.snapshot;
   g.escape_base = out->d_escape_base;
   g.heavy_list = w.heavy_list;
-  // CTAs per group: enough for one wave of record movers on small inputs
-  // (few groups), one per group on large ones
-  g.split = static_cast<uint32_t>(g.num_groups >= 512 ? 1 : (g.num_groups >= 64 ? 4 : 16));
+  // CTAs per group: >= ~2048 record movers in all, so escape-dense inputs
+  // (~1100 records per tile) keep enough loads in flight; sparse groups cost
+  // each extra CTA one 1 KiB tile-count load and an early exit
+  {
+    const uint64_t want = (2048 + g.num_groups - 1) / g.num_groups;
+    g.split = static_cast<uint32_t>(want < 1 ? 1 : (want > 64 ? 64 : want));
+  }
   g.heavy_pref = w.heavy_pref;
   g.heavy_count = w.heavy_count;
 
