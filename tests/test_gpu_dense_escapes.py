@@ -1,0 +1,147 @@
+"""Escape-dense streams (top-8 3-bit books put ~7% of real KV exponents
+outside the book; the handoff tests use 7.89%; all-escape chunks exist in
+the reference's own matrix): the encoder's staged-record path (K2a writers,
+K2b moves) and the decoder's K3e scatter + bitmap staging, checked against
+the CPU oracle section for section, bit for bit, and verdict for verdict on
+corrupted streams (exception class and chunk, codec.py:404-536)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sz_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+BOOKS = {0: (O.BF16_BOOK, O.BF16_ESC), 1: (O.E5M2_BOOK, O.E5M2_ESC),
+         2: (O.E4M3_BOOK, O.E4M3_ESC)}
+TILE = {0: 8192, 1: 16384, 2: 16384}   # decode tile (K4 / K3e)
+
+
+def sz():
+    import paper_2605_01708_b200 as m
+    return m
+
+
+def dense_case(fmt_id, n, rate, cb, seed):
+    bk, esc = BOOKS[fmt_id]
+    book_w = bk[:8] if cb == 3 else bk
+    words = O.exact_stream(fmt_id, n, rate, seed, book_w, esc)
+    return words, tuple(e for e, _ in book_w)
+
+
+def config(fmt_id, cb, chunk, book):
+    m = sz()
+    fmt = list(m.ElementFormat)[fmt_id]
+    return fmt, m.CodecConfig(fmt, cb, chunk_size=chunk, codebook=m.ExponentCodebook(
+        fmt, book, cb, m.CodebookMode.TOPK_EXPLICIT))
+
+
+CASES = [  # fmt, chunk, rate, code bits, n
+    (0, 1024, 0.0789, 4, 5 * 8192 + 333), (0, 1024, 0.0689, 3, 4 * 8192),
+    (0, 64, 0.2, 4, 3 * 8192 + 17), (0, 256, 0.03, 3, 6 * 8192 + 1),
+    (0, 8192, 0.5, 4, 2 * 8192 + 4095), (0, 4096, 0.009, 4, 8 * 8192 + 9),
+    (0, 1000, 0.07, 4, 3 * 8192 + 5),          # chunk not dividing the tile: stager path
+    (0, 16384, 0.07, 4, 5 * 8192),             # chunk larger than the decode tile
+    (1, 1024, 0.0789, 4, 3 * 16384 + 77), (1, 1024, 0.0689, 3, 4 * 16384),
+    (1, 16384, 0.3, 4, 2 * 16384 + 1), (1, 128, 0.05, 3, 3 * 16384 + 3),
+    (2, 1024, 0.07, 3, 3 * 16384 + 11), (2, 512, 1.0, 3, 16384 + 5),
+    # 3-bit top-8 BF16 tiles past the encoder's staged-record capacity (K2c)
+    (0, 1024, 0.16, 3, 4 * 16384 + 123),
+]
+
+
+@pytest.mark.parametrize("fmt_id,chunk,rate,cb,n", CASES)
+def test_dense_roundtrip_matches_oracle(fmt_id, chunk, rate, cb, n):
+    m = sz()
+    words, book = dense_case(fmt_id, n, rate, cb, 1000 + n % 97)
+    fmt, cfg = config(fmt_id, cb, chunk, book)
+    stream = m.RawTensorStream(fmt, torch.from_numpy(words).cuda())
+    enc = m.encode(stream, cfg)
+    ref = O.encode(words, O.Params(fmt_id, cb, False, chunk, False), book)
+    assert enc.n_escapes == ref["m"]
+    assert [b for _, b in enc.section_bytes()] == O.section_bytes(ref)
+    dec = m.decode(enc, cfg, enc.codebook)
+    assert torch.equal(dec.words, stream.words)
+    # the engine path: M stays on the device, K3e runs and each tile decides
+    from paper_2605_01708_b200.engine import DeviceCodec
+    eng = DeviceCodec(cfg, enc.codebook, n)
+    eng.ensure_capacity(stream.words)
+    out = eng.decode()
+    eng.check_status()
+    assert torch.equal(out, stream.words)
+
+
+def _mutations(sec, chunk, rng):
+    """(name, mutated sections) on an escape-dense stream: positions,
+    values and counts, at ordinals spread over the dense tiles."""
+    m_ = int(sec["m"])
+    pos, vals, counts = sec["escape_positions"], sec["escape_values"], sec["chunk_counts"]
+    out = []
+    for o in rng.choice(np.arange(1, m_), size=6, replace=False):
+        o = int(o)
+        p = pos.copy()
+        p[o] = p[o - 1]                         # not strictly increasing (or chunk start)
+        out.append((f"dup@{o}", dict(sec, escape_positions=p)))
+        p = pos.copy()
+        p[o] = chunk if pos.dtype == np.uint16 else 255
+        out.append((f"over@{o}", dict(sec, escape_positions=p)))
+        v = vals.copy()
+        v[o] = O.tables(sec["book"], sec["fmt"])[1][0]  # an in-book exponent
+        out.append((f"inbook@{o}", dict(sec, escape_values=v,
+                                        escape_values_packed=O.pack_le(v, O.FORMATS[sec["fmt"]][1]))))
+    k = int(rng.integers(0, counts.size - 1))
+    while counts[k] == 0:
+        k += 1
+    c = counts.copy()
+    c[k] -= 1
+    c[k + 1] += 1                               # an escape moved to the next chunk
+    out.append((f"shift@{k}", dict(sec, chunk_counts=c)))
+    p = pos.copy()
+    p[-1] = chunk - 1                           # last escape past the stream end (ragged tail)
+    out.append(("tail", dict(sec, escape_positions=p)))
+    return out
+
+
+@pytest.mark.parametrize("fmt_id,chunk,rate,cb,n", [
+    (0, 1024, 0.0789, 4, 5 * 8192 + 333), (0, 256, 0.05, 3, 3 * 8192 + 7),
+    (1, 1024, 0.0689, 3, 3 * 16384 + 77),
+])
+def test_dense_corruption_verdicts_match_oracle(fmt_id, chunk, rate, cb, n):
+    m = sz()
+    words, book = dense_case(fmt_id, n, rate, cb, 77 + n % 31)
+    fmt, cfg = config(fmt_id, cb, chunk, book)
+    p = O.Params(fmt_id, cb, False, chunk, False)
+    ref = O.encode(words, p, book)
+    ref = dict(ref, book=book, fmt=fmt_id)
+    rng = np.random.default_rng(n)
+    checked = 0
+    for name, sec in _mutations(ref, chunk, rng):
+        try:
+            O.decode(sec, p, book)
+            want = None
+        except O.OracleCorruption as exc:
+            want = exc.chunk
+        cb_book = cfg.codebook
+        streams = m.EncodedStreams(
+            n, int(sec["m"]), sec["packed_codes"], sec["sign_mantissa"], sec["chunk_counts"],
+            sec["escape_positions"], sec["escape_values"], cb_book)
+        dev = m.EncodedStreams(
+            n, int(sec["m"]), torch.from_numpy(np.frombuffer(sec["packed_codes"], np.uint8).copy()).cuda(),
+            torch.from_numpy(np.frombuffer(sec["sign_mantissa"], np.uint8).copy()).cuda(),
+            torch.from_numpy(sec["chunk_counts"].astype(np.uint32)).cuda(),
+            torch.from_numpy(np.ascontiguousarray(sec["escape_positions"])).cuda(),
+            torch.from_numpy(np.ascontiguousarray(sec["escape_values"])).cuda(), cb_book)
+        for s_ in (streams, dev):
+            if want is None:
+                out = m.decode(s_, cfg, cb_book).words
+                out = out.cpu().numpy() if isinstance(out, torch.Tensor) else out
+                assert np.array_equal(out, O.decode(sec, p, book)), name
+            else:
+                with pytest.raises(m.CorruptionError) as exc:
+                    m.decode(s_, cfg, cb_book)
+                assert exc.value.chunk == want, name
+        checked += want is not None
+    assert checked >= 10
