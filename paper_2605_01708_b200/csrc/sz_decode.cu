@@ -22,6 +22,8 @@
 // Corruption never faults: every index is bounds-checked, and each failed
 // check records its smallest offending ordinal/element in sz_decode_status;
 // the host raises CorruptionError in the reference's check order.
+#include <cstdlib>
+#include <type_traits>
 #include "sz_common.cuh"
 #include "sz_scan.cuh"
 
@@ -181,6 +183,232 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+template <int POSB>
+__device__ __forceinline__ uint64_t load_pos(const void* p, uint64_t o) {
+  if constexpr (POSB == 1) return static_cast<const uint8_t*>(p)[o];
+  else if constexpr (POSB == 2) return static_cast<const uint16_t*>(p)[o];
+  else return static_cast<const uint32_t*>(p)[o];
+}
+
+// ------------------------------------------------------------------ K3e
+// Escape-dense chunk-relative streams (codec.py:509-536, ε of a few %, e.g.
+// top-8 3-bit books at ~7%): the per-ordinal position work moves out of the
+// decoder's stagers into a flat pass.  One warp per 16384-element window:
+//   - the window's chunk offsets (K3) in shared memory, ordinals in rounds of
+//     32 with the next 4 rounds' positions / values in flight, each lane's
+//     chunk found from the previous round's (one compare when a round crosses
+//     at most one chunk start);
+//   - every per-ordinal check of _escape_indices and the value checks
+//     (codec.py:451-457, 515-535), first offending ordinal per check;
+//   - the window's element escape bitmap built with shared-memory ORs and
+//     written once with 16-byte stores, and the escape count of every decode
+//     tile in it (popc of its words).
+// The decoder then stages a tile exactly like sentinel mode: its bitmap words
+// (coalesced), a warp scan for each slot's first compact index, and its
+// values as one contiguous run from the scanned tile counts.  Windows are a
+// multiple of every decode tile, so every bitmap word and tile count has one
+// writer (no atomics in global memory, no zeroing pass).
+constexpr int kMarkWin = 16384;
+constexpr int kMarkWinWords = kMarkWin / 32;
+constexpr int kMarkWarps = 8;
+constexpr uint32_t kMarkMinChunk = 32;                        // dense path needs chunk >= 32
+constexpr int kMarkMaxChunks = kMarkWin / kMarkMinChunk + 2;  // chunks touching a window, + end
+
+struct MarkArgs {
+  const uint64_t* m_ptr;
+  uint64_t m;
+  const uint64_t* offsets;   // chunk ordinal offsets (K3), n_chunks + 1
+  const void* positions;
+  const uint8_t* values;
+  uint64_t n, n_windows;
+  uint64_t n_words;          // bitmap words = decode tiles x tile_words
+  uint32_t chunk, tile_words, exp_bins;
+  uint32_t esc_ok[8];        // valid escape values (not in the book) as a 256-bit set
+  uint32_t* mark_bits;
+  uint32_t* tile_marks;
+  sz_decode_status* status;
+};
+
+struct alignas(16) MarkSmem {
+  uint32_t bits[kMarkWinWords];
+  uint32_t srel[kMarkMaxChunks];   // chunk starts as ordinals relative to the window's first
+};
+static_assert(sizeof(MarkSmem) % 16 == 0, "per-warp K3e state stays 16-byte aligned");
+
+template <int POSB>
+__global__ void __launch_bounds__(kMarkWarps * 32) escape_marks_kernel(const MarkArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int lane = threadIdx.x & 31;
+  MarkSmem& S = reinterpret_cast<MarkSmem*>(smem_raw)[threadIdx.x >> 5];
+  __shared__ uint32_t s_esc_ok[8];
+  pdl_trigger();
+  if (threadIdx.x < 8) s_esc_ok[threadIdx.x] = a.esc_ok[threadIdx.x];
+  for (int i = lane; i < kMarkWinWords / 4; i += 32)
+    reinterpret_cast<uint4*>(S.bits)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  pdl_wait();
+  const uint64_t m = a.m_ptr ? min(*a.m_ptr, a.m) : a.m;
+  const uint64_t chunk = a.chunk;
+  const uint64_t gw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w = gw; w < a.n_windows; w += nw) {
+    const uint64_t e0 = w * kMarkWin, e1 = min(e0 + kMarkWin, a.n);
+    const uint64_t ka = e0 / chunk;
+    const uint32_t nk = static_cast<uint32_t>((e1 - 1) / chunk - ka + 1);  // chunks in the window
+    const uint64_t* const offk = a.offsets + ka;
+    const uint64_t o_lo = min(offk[0], m), o_hi = max(min(offk[nk], m), o_lo);
+    const uint64_t n_o = o_hi - o_lo;
+    // window-relative element of chunk ka's start (<= 0) and the bounds of
+    // a hit / of the stream, in 32-bit arithmetic
+    const int32_t kbase = static_cast<int32_t>(static_cast<int64_t>(ka * chunk) -
+                                               static_cast<int64_t>(e0));
+    const uint32_t span = static_cast<uint32_t>(e1 - e0);
+    const int32_t past = static_cast<int32_t>(min(a.n - e0, static_cast<uint64_t>(0x7FFFFFFF)));
+    if (n_o < (1ull << 31)) {
+      // Fast path: the window's chunk starts as u32 ordinals relative to o_lo
+      uint32_t* const srel = S.srel;
+      for (uint32_t i = lane; i <= nk; i += 32)
+        srel[i] = static_cast<uint32_t>(max(min(offk[i], m), o_lo) - o_lo);
+      __syncwarp();
+      const uint32_t no = static_cast<uint32_t>(n_o);
+      using PosT = typename std::conditional<POSB == 1, uint8_t, uint16_t>::type;
+      const PosT* const pos_w = static_cast<const PosT*>(a.positions) + o_lo;
+      const uint8_t* const val_w = a.values + o_lo;
+      const uint32_t chunk32 = a.chunk;
+      // Rounds of 32 consecutive ordinals (coalesced loads, the next 4
+      // rounds' in flight); each round's chunks from the previous round's
+      // (one compare when it crosses at most one chunk start).  (A variant
+      // staging each lane's contiguous slice in shared memory and walking it
+      // with a running chunk index issued fewer loads but measured 2x slower:
+      // its per-ordinal branches and the staging stores' load latency.)
+      constexpr int U = 4;
+      uint32_t cur = 0;          // srel[cur] <= the round's first ordinal
+      uint32_t carry_pv = 0;     // position of the previous round's last ordinal
+      uint32_t carry_k = ~0u;    // and its chunk (none before the first round)
+      uint32_t pvs[U], vs[U];
+      auto load_batch = [&](uint32_t b0, uint32_t (&pp)[U], uint32_t (&vv)[U]) {
+        const PosT* const pb = pos_w + b0 + lane;
+        const uint8_t* const vb = val_w + b0 + lane;
+        const uint32_t left = no - b0 - lane;  // > 32u exactly when ordinal 32u + lane exists
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool in = static_cast<int32_t>(left) > 32 * u;
+          pp[u] = in ? static_cast<uint32_t>(pb[32 * u]) : 0u;
+          vv[u] = in ? static_cast<uint32_t>(vb[32 * u]) : 0u;
+        }
+      };
+      if (no) load_batch(0, pvs, vs);
+      for (uint32_t b0 = 0; b0 < no; b0 += 32 * U) {
+        uint32_t npvs[U], nvs[U];
+        if (b0 + 32 * U < no) load_batch(b0 + 32 * U, npvs, nvs);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t br = b0 + 32 * u;
+          if (br >= no) break;
+          const uint32_t orl = br + lane, last = min(br + 31, no - 1);
+          const uint32_t pv = pvs[u], v = vs[u];
+          uint32_t k = cur;
+          const bool multi = cur + 2 <= nk && srel[cur + 2] <= last;  // (warp-uniform)
+          if (__builtin_expect(multi, 0)) {
+            uint32_t hi = nk;
+            while (hi - k > 1) {
+              const uint32_t mid = (k + hi) >> 1;
+              if (srel[mid] <= orl) k = mid; else hi = mid;
+            }
+          } else {
+            k += cur + 1 < nk && srel[cur + 1] <= orl ? 1u : 0u;
+          }
+          // an ordinal is its chunk's first exactly when its predecessor is
+          // in another chunk (offsets are monotone)
+          uint32_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
+          uint32_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
+          if (lane == 0) {
+            kprev = carry_k;
+            prev = carry_pv;
+          }
+          cur = __shfl_sync(0xffffffffu, k, 31);
+          carry_k = cur;
+          carry_pv = __shfl_sync(0xffffffffu, pv, 31);
+          const int32_t rel = kbase + static_cast<int32_t>(k * chunk32 + pv);
+          const bool live = orl < no;
+          // one set test covers the domain and the in-book check
+          const bool val_ok = (s_esc_ok[v >> 5] >> (v & 31)) & 1u;
+          const bool over = pv >= chunk32, beyond = rel >= past;
+          const bool not_inc = k == kprev && prev >= pv;
+          if (__builtin_expect(live && (!val_ok || over || beyond || not_inc), 0)) {
+            // rare: the reference's checks in order (codec.py:446-536)
+            const uint64_t o = o_lo + orl;
+            if (v >= a.exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+            else if (!val_ok) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+            if (over) record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+            else if (beyond) record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+            else if (not_inc) record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+          }
+          if (live && !over && static_cast<uint32_t>(rel) < span)
+            atomicOr(&S.bits[static_cast<uint32_t>(rel) >> 5], 1u << (rel & 31));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          pvs[u] = npvs[u];
+          vs[u] = nvs[u];
+        }
+      }
+    } else {
+      // corrupt counts (> 2^31 ordinals in one window): plain per-ordinal
+      // loop in 64-bit arithmetic, same checks
+      for (uint64_t o = o_lo + lane; o < o_hi; o += 32) {
+        uint32_t lo = 0, hi = nk;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (min(offk[mid], m) <= o) lo = mid; else hi = mid;
+        }
+        const uint32_t pv = static_cast<uint32_t>(load_pos<POSB>(a.positions, o));
+        const uint32_t v = a.values[o];
+        const uint64_t idx = (ka + lo) * chunk + pv;
+        const bool in_book = !((s_esc_ok[v >> 5] >> (v & 31)) & 1u);
+        if (v >= a.exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+        else if (in_book) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+        if (pv >= chunk) {
+          record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+        } else if (idx >= a.n) {
+          record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+        } else {
+          if (o > min(offk[lo], m) && static_cast<uint32_t>(load_pos<POSB>(a.positions, o - 1)) >= pv)
+            record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+          if (idx >= e0 && idx < e1) {
+            const uint32_t r = static_cast<uint32_t>(idx - e0);
+            atomicOr(&S.bits[r >> 5], 1u << (r & 31));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // flush: 16-byte stores of the window's words, each decode tile's count,
+    // and the shared words zeroed for the next window
+    const uint64_t wd0 = e0 / 32;
+    const uint32_t pieces_per_tile = a.tile_words / 128;   // 128 words per round of 32 lanes
+    uint32_t tsum = 0;
+#pragma unroll
+    for (int j = 0; j < kMarkWinWords / 128; ++j) {
+      uint4* sq = reinterpret_cast<uint4*>(S.bits) + lane + 32 * j;
+      const uint4 q = *sq;
+      *sq = make_uint4(0, 0, 0, 0);
+      const uint64_t wd = wd0 + 4ull * (lane + 32 * j);
+      if (wd + 4 <= a.n_words) *reinterpret_cast<uint4*>(a.mark_bits + wd) = q;
+      uint32_t c = __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+      tsum += c;
+      if ((j + 1) % pieces_per_tile == 0) {
+        const uint64_t tile = (wd0 + 128ull * (j + 1) - 1) / a.tile_words;
+        if (lane == 0 && tile * a.tile_words < a.n_words) a.tile_marks[tile] = tsum;
+        tsum = 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ K4
 struct DecodeArgs {
   const uint64_t* m_ptr;     // optional device-resident M
@@ -235,13 +463,6 @@ __device__ __forceinline__ void ld_packed(const uint8_t* src, uint32_t* w) {
   }
 }
 
-template <int POSB>
-__device__ __forceinline__ uint64_t load_pos(const void* p, uint64_t o) {
-  if constexpr (POSB == 1) return static_cast<const uint8_t*>(p)[o];
-  else if constexpr (POSB == 2) return static_cast<const uint16_t*>(p)[o];
-  else return static_cast<const uint32_t*>(p)[o];
-}
-
 template <int FMT>
 __device__ __forceinline__ void rebuild_group(uint32_t e4, uint32_t a4, uint32_t* outw, int g) {
   if constexpr (FMT == SZ_BF16) {
@@ -288,6 +509,27 @@ __device__ __forceinline__ uint32_t escape_value(const uint8_t* vals, uint32_t f
   return ofirst + c < m ? gvals[ofirst + c] : 0u;
 }
 
+// Escape overwrite of one 4-element group without a per-escape loop.  The
+// group's escape bits mg (4 bits) select, through one PRMT, bytes of the
+// 4-byte window of staged values starting at the group's first rank r
+// (values are compact in element order) in place of the dense exponent
+// bytes: selector nibble k = rank of element k among the group's escapes
+// when bit k is set, else 4 + k (keep).  The selectors of all 16 patterns
+// sit in shared memory.  Explicit modes also check the escaped elements'
+// dense codes (codec.py:472-476): an in-range code is 0 exactly when its
+// exponent is the book's first entry (entries are distinct; out-of-range
+// codes are CODE_RANGE, an earlier check).  Returns the updated bytes;
+// *nondummy gets the mask of escaped bytes whose exponent is not entry 0.
+__device__ __forceinline__ uint32_t merge_group(uint32_t e4, uint32_t mg, uint32_t r,
+                                                uint32_t vals_base, uint32_t sel_base,
+                                                uint32_t keep4, uint32_t* nondummy) {
+  const uint32_t sel = lds_u32(sel_base + 4 * mg);
+  const uint32_t a0 = vals_base + (r & ~3u);
+  const uint32_t v4 = __funnelshift_r(lds_u32(a0), lds_u32(a0 + 4), 8 * (r & 3));
+  *nondummy = (e4 ^ keep4) & __byte_perm(0xFFFFFFFFu, 0u, sel);
+  return __byte_perm(v4, e4, sel);
+}
+
 // ------------------------------------------------------------------ K4 (persistent)
 // Explicit modes (chunk-relative and abs32).  Same warp-specialised shape as
 // the encoder: warp 8 streams each tile's code and sign|mantissa planes into a
@@ -296,6 +538,7 @@ __device__ __forceinline__ uint32_t escape_value(const uint8_t* vals, uint32_t f
 // decode slots from smem and write 256-bit stores.  No CTA-wide barriers in
 // steady state — only mbarrier hand-offs.
 constexpr int kDecHelpers = 3;                          // escape-staging warps
+constexpr int kPosMarked = 8;   // K4 POSB of escape-dense chunk-relative streams (K3e)
 constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
 constexpr int kDecOffStage = 64;                        // staged chunk offsets per helper
 template <int FMT>
@@ -307,7 +550,9 @@ struct DecSmem {
   alignas(128) uint8_t sm[STAGES][TILE * Fmt<FMT>::kSmBits / 8];
   uint32_t bitmap[STAGES][TILE / 32];
   uint32_t slot_first[STAGES][kDecSlots];  // compact index of a slot's first escape
-  uint8_t vals[STAGES][kDecValCap<FMT>];   // escape values by (ordinal - ofirst)
+  // escape values by (ordinal - ofirst); 8 bytes of slack for the decode
+  // warps' 4-byte window reads (merge_group) at the end of the run
+  alignas(16) uint8_t vals[STAGES][kDecValCap<FMT> + 8];
   uint64_t ofirst[STAGES];                 // ordinal of the tile's first escape
   uint64_t off[kDecHelpers][kDecOffStage + 1];
   uint64_t meta[STAGES];
@@ -331,6 +576,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   constexpr uint64_t TILE = static_cast<uint64_t>(kDecSlots) * EPV;
   constexpr bool ABS = POSB == 4;
   constexpr bool SENT = POSB == 0;   // sentinel mode: marks in the code plane
+  // escape bitmap + tile ordinal bases from a pre-pass: K3s (sentinel) or
+  // K3e (escape-dense chunk-relative streams, POSB == kPosMarked)
+  constexpr bool MARKED = SENT || POSB == kPosMarked;
+  // escape-dense streams (the K3e path): escapes merged group by group
+  // (merge_group) instead of the per-escape loop, which serialises a warp
+  // on its densest slot; sparse streams keep the loop (smaller code, ~1
+  // escape per warp round)
+  constexpr bool kGroupMerge = POSB == kPosMarked;
   constexpr int LUT2 = CB == 4 ? 256 : 64;
   constexpr uint32_t kCodeMask = (1u << CB) - 1;
   using Smem = DecSmem<FMT>;
@@ -359,6 +612,18 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     s_inbook[tid] = w;
   }
   auto in_book = [&](uint32_t v) { return (s_inbook[v >> 5] >> (v & 31)) & 1u; };
+  // merge_group's PRMT selectors, one per 4-bit escape pattern
+  __shared__ uint32_t s_sel[16];
+  if (tid < 16) {
+    uint32_t sel = 0, rank = 0;
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t nib = (tid >> k) & 1 ? rank++ : 4u + k;
+      sel |= nib << (4 * k);
+    }
+    s_sel[tid] = sel;
+  }
+  const uint32_t sel_base = smem_addr(s_sel);
+  const uint32_t d0 = p.dec_lut[0];   // exponent of dense code 0 (the dummy)
   // E5M2 with 4-bit codes: a pair table indexed by a code byte (elements
   // 2i, 2i+1) whose u16 entries hold both exponents already at their E5M2
   // bit positions (bits 2-6 of each byte) — reconstruct (formats.py:136-155)
@@ -436,7 +701,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       // Direct happens-before with the decode warps' last use of this stage
       // (already guaranteed through the producer's chain; free to re-check).
       mbar_wait(&S.empty[s], ph ^ 1);
-      if constexpr (!SENT) {  // (sentinel staging writes every bitmap word itself)
+      if constexpr (!MARKED) {  // (marked staging writes every bitmap word itself)
 #pragma unroll
         for (int i = lane; i < static_cast<int>(TILE / 32); i += 32) S.bitmap[s][i] = 0;
 #pragma unroll
@@ -478,14 +743,37 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
       }
       __syncwarp();
-      if constexpr (SENT) {
-        // Sentinel mode (codec.py:459-467): the tile's marks come from its
-        // code plane (landed in shared memory), its first ordinal from the
-        // K3s scan; the staging is then exactly explicit mode's.
+      if constexpr (MARKED) {
+        // Sentinel mode (codec.py:459-467): the tile's marks come from K3s's
+        // scan of its code plane; escape-dense chunk-relative mode: from
+        // K3e's walk over the positions.  Its first ordinal is the scan of
+        // the per-tile counts.
         const uint64_t t_first = a.offsets[tile];
         const uint64_t t_end = max(a.offsets[tile + 1], t_first);
         o_first = t_first;
-        {
+        if constexpr (!SENT) {
+          // K3e checked every value already: a plain copy of the tile's run
+          // (4-byte loads of the words inside [t_first, t_end), bytes at the ends)
+          const uint64_t o_hi = min(min(t_end, m), t_first + kDecValCap<FMT>);
+          const uint64_t w_lo = (t_first + 3) >> 2, w_hi = o_hi >> 2;
+          if (w_lo < w_hi && !(reinterpret_cast<uintptr_t>(a.values) & 3)) {
+            const uint32_t* vw = reinterpret_cast<const uint32_t*>(a.values);
+            for (uint64_t i = w_lo + lane; i < w_hi; i += 32) {
+              const uint32_t q = vw[i];
+              const uint32_t c = static_cast<uint32_t>(4 * i - t_first);
+              S.vals[s][c] = static_cast<uint8_t>(q);
+              S.vals[s][c + 1] = static_cast<uint8_t>(q >> 8);
+              S.vals[s][c + 2] = static_cast<uint8_t>(q >> 16);
+              S.vals[s][c + 3] = static_cast<uint8_t>(q >> 24);
+            }
+            if (lane < 3 && t_first + lane < 4 * w_lo)
+              S.vals[s][lane] = a.values[t_first + lane];
+            if (lane >= 3 && lane < 6 && 4 * w_hi + (lane - 3) < o_hi)
+              S.vals[s][4 * w_hi + (lane - 3) - t_first] = a.values[4 * w_hi + (lane - 3)];
+          } else {
+            for (uint64_t o = t_first + lane; o < o_hi; o += 32) S.vals[s][o - t_first] = a.values[o];
+          }
+        } else {
           // the tile's values first — staged (first kDecValCap) and checked
           // (codec.py:446-457) for every ordinal its marks reach — while its
           // code plane is still in flight
@@ -796,6 +1084,28 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
         uint32_t bm = S.bitmap[s][slot];
         const uint32_t bm0 = bm;
+        const uint32_t first = kGroupMerge && bm ? S.slot_first[s][slot] : 0u;
+        if (kGroupMerge && bm && first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
+          // group-wise PRMT merge of the placed exponent fields (bits 2-6)
+          const uint32_t vbase = smem_addr(S.vals[s]);
+          uint32_t r = first, nd_any = 0;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t mg = (bm >> (4 * g)) & 15u;
+            if (mg) {
+              uint32_t nd;
+              const uint32_t t = merge_group(ow[g] >> 2 & 0x1F1F1F1Fu, mg, r, vbase, sel_base,
+                                             d0 * 0x01010101u, &nd);
+              ow[g] = (ow[g] & 0x83838383u) | ((t << 2) & 0x7C7C7C7Cu);
+              if (!SENT && nd && !nd_any) {
+                record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + 4 * g + (__ffs(nd) - 1) / 8);
+                nd_any = 1;
+              }
+              r += __popc(mg);
+            }
+          }
+          bm = 0;
+        }
         while (bm) {  // rare: overwrite escaped exponent fields (bits 2-6 of the byte)
           const int j = __ffs(bm) - 1;
           bm &= bm - 1;
@@ -850,7 +1160,29 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       if constexpr (EPV == 32) bm = S.bitmap[s][slot];
       else bm = (S.bitmap[s][slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
       const uint32_t bm0 = bm;
-      // rare: overwrite escaped exponents (compact loop over set bits; the
+      const uint32_t first = kGroupMerge && bm ? S.slot_first[s][slot] : 0u;
+      if (kGroupMerge && bm && first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
+        // escaped exponents merged group by group (merge_group): no loop
+        // over the escapes, so escape-dense slots do not serialise the warp
+        const uint32_t vbase = smem_addr(S.vals[s]);
+        uint32_t r = first, nd_any = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t mg = (bm >> (4 * g)) & 15u;
+          if (mg) {
+            uint32_t nd;
+            eg[g] = merge_group(eg[g], mg, r, vbase, sel_base, d0 * 0x01010101u, &nd);
+            if (!SENT && nd && !nd_any) {
+              record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + 4 * g + (__ffs(nd) - 1) / 8);
+              nd_any = 1;
+            }
+            r += __popc(mg);
+          }
+        }
+        bm = 0;
+      }
+      // beyond the staged values (tiles with more escapes than kDecValCap):
+      // the compact loop over set bits, values from global memory (the
       // register arrays are indexed through selects, never dynamically)
       while (bm) {
         const int j = __ffs(bm) - 1;
@@ -911,44 +1243,113 @@ struct DecodeWs {
   unsigned long long* off_counter;
   uint64_t* dec_states;
   unsigned long long* dec_counter;
-  uint32_t* tile_marks;  // sentinel: marks per decode tile
-  uint32_t* mark_bits;   // sentinel: one bit per element (K3s), read by the stagers
+  uint64_t* t_states;    // marked (K3e): look-back states of the tile-count scan
+  unsigned long long* t_counter;
+  uint64_t* tile_offsets;  // marked (K3e): first ordinal of every decode tile
+  uint32_t* tile_marks;  // sentinel / marked: escapes per decode tile
+  uint32_t* mark_bits;   // sentinel / marked: one bit per element, read by the stagers
   size_t zero_bytes;  // prefix of the workspace that must be zeroed
   size_t total;
 };
 
-DecodeWs carve(void* base, uint64_t n, const sz_params* p) {
+// Escape-dense chunk-relative streams take the K3e path (bitmap pre-pass)
+// when the declared M reaches 1/kDenseDiv of N.  The crossover was measured
+// with SZ_DEC_MARKED=0/1 (forces either path; tuning and tests only) at 2^31
+// words (profiles/bench_dense_r02.jsonl): the stager walk wins up to ~2.4%
+// escapes, K3e from ~4% (BF16 7.89%: 1227 -> 1720 GB/s).
+constexpr uint64_t kDenseDiv = 32;
+int marked_override() {
+  const char* e = getenv("SZ_DEC_MARKED");   // read per call: tests force both paths
+  return e && *e ? atoi(e) : -1;
+}
+bool want_marked(uint64_t n, uint64_t m, const sz_params* p) {
+  if (p->sentinel || p->abs32 || p->chunk_size < kMarkMinChunk || m == 0) return false;
+  const int o = marked_override();
+  if (o >= 0) return o != 0;
+  return m * kDenseDiv >= n;
+}
+
+DecodeWs carve(void* base, uint64_t n, const sz_params* p, bool marked) {
   DecodeWs w{};
   const bool chunked = !p->sentinel && !p->abs32;
-  const uint64_t dtiles = (n + decode_tile_for(p->fmt) - 1) / decode_tile_for(p->fmt);
+  const uint64_t tile = decode_tile_for(p->fmt);
+  const uint64_t dtiles = (n + tile - 1) / tile;
   // scanned counts: per-chunk escape counts, or (sentinel) per-tile marks
   // abs32: the scanned array is replaced by per-tile ordinal bounds (K3a)
   const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size
                                    : (p->sentinel ? dtiles : 0);
   const uint64_t nbounds = p->abs32 ? dtiles + 1 : 0;
   const uint64_t otiles = nchunks ? offsets_tiles(nchunks) : 0;
-  uint64_t* b = static_cast<uint64_t*>(base);
-  // zeroed region first: look-back states + counters
-  w.off_states = b;
-  w.off_counter = reinterpret_cast<unsigned long long*>(b + otiles);
-  w.dec_states = b + otiles + 1;
-  w.dec_counter = reinterpret_cast<unsigned long long*>(b + otiles + 1 + dtiles);
-  // offsets start 16-byte aligned (the scan's vector stores; the workspace
-  // base is 256-aligned); abs32 bounds sit inside the zeroed prefix
-  const uint64_t off0 = (otiles + dtiles + 2 + 1) & ~1ull;
-  w.zero_bytes = (off0 + nbounds) * sizeof(uint64_t);
-  w.offsets = b + off0;
-  w.tile_marks = reinterpret_cast<uint32_t*>(w.offsets + (nchunks ? nchunks + 1 : nbounds));
+  const uint64_t ttiles = marked ? offsets_tiles(dtiles) : 0;
+  // layout in u64 units from the (256-aligned) base; zeroed region first:
+  // look-back states + counters (+ abs32 bounds)
+  uint64_t at = 0;
+  const uint64_t i_off_states = at; at += otiles;
+  const uint64_t i_off_counter = at; at += 1;
+  const uint64_t i_dec_states = at; at += dtiles;
+  const uint64_t i_dec_counter = at; at += 1;
+  const uint64_t i_t_states = at; at += ttiles;
+  const uint64_t i_t_counter = at; at += marked ? 1 : 0;
+  // offsets start 16-byte aligned (the scan's vector stores)
+  at = (at + 1) & ~1ull;
+  const uint64_t i_offsets = at;
+  at += nbounds;
+  w.zero_bytes = at * sizeof(uint64_t);
+  at = i_offsets + (nchunks ? nchunks + 1 : nbounds);
+  at = (at + 1) & ~1ull;
+  const uint64_t i_tile_offsets = at; at += marked ? dtiles + 1 : 0;
+  const bool marks = p->sentinel || marked;
+  const uint64_t tm_bytes = marks ? dtiles * sizeof(uint32_t) : 0;
+  const uint64_t b_tile_marks = at * sizeof(uint64_t);
   // (16-byte aligned: the stagers read it with vector loads)
-  const uintptr_t mb = reinterpret_cast<uintptr_t>(w.tile_marks + (p->sentinel ? dtiles : 0));
-  w.mark_bits = reinterpret_cast<uint32_t*>((mb + 15) & ~static_cast<uintptr_t>(15));
-  const uint64_t nbits_words = p->sentinel ? dtiles * (decode_tile_for(p->fmt) / 32) : 0;
-  w.total = w.zero_bytes + (nchunks ? (nchunks + 1) * sizeof(uint64_t) : 0) +
-            (p->sentinel ? dtiles * sizeof(uint32_t) + 16 + nbits_words * sizeof(uint32_t) : 0) +
-            256;
+  const uint64_t b_mark_bits = (b_tile_marks + tm_bytes + 15) & ~15ull;
+  const uint64_t nbits_words = marks ? dtiles * (tile / 32) : 0;
+  w.total = b_mark_bits + nbits_words * sizeof(uint32_t) + 256;
+  uint8_t* b8 = static_cast<uint8_t*>(base);
+  uint64_t* b = static_cast<uint64_t*>(base);
+  w.off_states = b + i_off_states;
+  w.off_counter = reinterpret_cast<unsigned long long*>(b + i_off_counter);
+  w.dec_states = b + i_dec_states;
+  w.dec_counter = reinterpret_cast<unsigned long long*>(b + i_dec_counter);
+  w.t_states = b + i_t_states;
+  w.t_counter = reinterpret_cast<unsigned long long*>(b + i_t_counter);
+  w.offsets = b + i_offsets;
+  w.tile_offsets = b + i_tile_offsets;
+  w.tile_marks = reinterpret_cast<uint32_t*>(b8 + b_tile_marks);
+  w.mark_bits = reinterpret_cast<uint32_t*>(b8 + b_mark_bits);
   return w;
 }
 
+// Exclusive scan of n u32 counts into u64 offsets (K3's kernels): decoupled
+// look-back up to 32 CTAs, reduce-then-scan beyond.
+cudaError_t launch_scan(OffsetsArgs oa, cudaStream_t s) {
+  oa.num_tiles = offsets_tiles(oa.n_counts);
+  cudaError_t e = cudaSuccess;
+  if (oa.num_tiles > 32) {
+    // many CTAs: per-CTA sums in the look-back state array (unused then)
+    e = launch_pdl(offsets_sums_kernel, dim3(static_cast<unsigned>(oa.num_tiles)),
+                   dim3(kThreads), 0, s, oa, oa.states);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    oa.sums = oa.states;
+  }
+  e = launch_pdl(offsets_kernel, dim3(static_cast<unsigned>(oa.num_tiles)), dim3(kThreads), 0,
+                 s, oa);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+template <int POSB>
+cudaError_t launch_marks(const MarkArgs& ma, cudaStream_t s) {
+  auto kern = escape_marks_kernel<POSB>;
+  const int smem = static_cast<int>(sizeof(MarkSmem)) * kMarkWarps;
+  const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kMarkWarps * 32);
+  if (ks.err != cudaSuccess) return ks.err;
+  const uint64_t want = static_cast<uint64_t>(ks.sms) * (ks.per_sm < 1 ? 1 : ks.per_sm);
+  const uint64_t ctas = (ma.n_windows + kMarkWarps - 1) / kMarkWarps;
+  const unsigned grid = static_cast<unsigned>(ctas < want ? ctas : want);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kMarkWarps * 32), smem, s, ma);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
 
 // Explicit modes: persistent warp-specialised kernel.
 template <int FMT, int CB, int POSB>
@@ -969,6 +1370,7 @@ cudaError_t dec_pos(int posb, const sz_params& p, const DecodeArgs& a, cudaStrea
     case 0: return launch_persistent<FMT, CB, 0>(p, a, s);
     case 1: return launch_persistent<FMT, CB, 1>(p, a, s);
     case 2: return launch_persistent<FMT, CB, 2>(p, a, s);
+    case kPosMarked: return launch_persistent<FMT, CB, kPosMarked>(p, a, s);
     default: return launch_persistent<FMT, CB, 4>(p, a, s);
   }
 }
@@ -985,9 +1387,8 @@ int sz_record_cuda(cudaError_t e);
 int sz_check_params(const sz_params* p, int decode_side);
 
 size_t sz_decode_workspace_bytes(uint64_t n, uint64_t m, const sz_params* p) {
-  (void)m;
   if (!p || p->fmt > SZ_E4M3 || p->chunk_size == 0) return 0;
-  return carve(nullptr, n, p).total;
+  return carve(nullptr, n, p, want_marked(n, m, p)).total;
 }
 
 }  // extern "C"
@@ -1010,11 +1411,14 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   if ((reinterpret_cast<uintptr_t>(d_words_out) & 31) ||
       (reinterpret_cast<uintptr_t>(in->d_codes) & 15) || (reinterpret_cast<uintptr_t>(in->d_sm) & 15))
     return SZ_EALIGN;
-  if (ws_bytes < sz_decode_workspace_bytes(n, m, p)) return SZ_EWORKSPACE;
+  // the escape-dense path when the workspace was sized for it (a caller may
+  // size it with another M than the one declared here)
+  const bool marked = want_marked(n, m, p) && ws_bytes >= carve(nullptr, n, p, true).total;
+  if (ws_bytes < carve(nullptr, n, p, marked).total) return SZ_EWORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool chunked = !p->sentinel && !p->abs32;
   const int sm_bits = p->fmt == SZ_BF16 ? 8 : (p->fmt == SZ_E5M2 ? 3 : 4);
-  DecodeWs w = carve(d_ws, n, p);
+  DecodeWs w = carve(d_ws, n, p, marked);
   const uint64_t nchunks = chunked ? (n + p->chunk_size - 1) / p->chunk_size : 0;
   if (chunked && in->n_counts != nchunks) return SZ_ECONFIG;  // host raises first
   if (!in->d_n_escapes && m && (!in->d_values || (!p->sentinel && !in->d_positions)))
@@ -1056,26 +1460,45 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
     oa.m_ptr = in->d_n_escapes;
     oa.counts = p->sentinel ? w.tile_marks : in->d_counts;
     oa.sentinel = p->sentinel ? 1 : 0;
-    const uint64_t ncounts = p->sentinel ? dtiles : nchunks;
-    oa.n_counts = ncounts;
+    oa.n_counts = p->sentinel ? dtiles : nchunks;
     oa.m = m;
     oa.offsets = w.offsets;
     oa.states = w.off_states;
     oa.tile_counter = w.off_counter;
-    oa.num_tiles = offsets_tiles(ncounts);
     oa.status = d_status;
-    if (oa.num_tiles > 32) {
-      // many CTAs: reduce-then-scan (per-CTA sums in the look-back state
-      // array, unused then) instead of a look-back chain across CTAs
-      e = launch_pdl(offsets_sums_kernel, dim3(static_cast<unsigned>(oa.num_tiles)),
-                     dim3(kThreads), 0, s, oa, w.off_states);
-      if (e == cudaSuccess) e = cudaGetLastError();
-      if (e != cudaSuccess) return sz_record_cuda(e);
-      oa.sums = w.off_states;
-    }
-    e = launch_pdl(offsets_kernel, dim3(static_cast<unsigned>(oa.num_tiles)), dim3(kThreads), 0,
-                   s, oa);
-    if (e == cudaSuccess) e = cudaGetLastError();
+    e = launch_scan(oa, s);
+    if (e != cudaSuccess) return sz_record_cuda(e);
+  }
+  if (marked) {
+    // K3e: escape bitmap + per-tile counts + every per-ordinal check, then
+    // the tile counts' scan (first ordinal of every decode tile)
+    MarkArgs ma{};
+    ma.m_ptr = in->d_n_escapes;
+    ma.m = m;
+    ma.offsets = w.offsets;
+    ma.positions = in->d_positions;
+    ma.values = in->d_values;
+    ma.n = n;
+    ma.n_windows = (n + kMarkWin - 1) / kMarkWin;
+    ma.chunk = p->chunk_size;
+    ma.tile_words = static_cast<uint32_t>(decode_tile_for(p->fmt) / 32);
+    ma.n_words = dtiles * ma.tile_words;
+    ma.exp_bins = 1u << (p->fmt == SZ_BF16 ? 8 : (p->fmt == SZ_E5M2 ? 5 : 4));
+    // valid escape values: inside the exponent domain and outside the book
+    for (uint32_t i = 0; i < ma.exp_bins && i < 256; ++i)
+      ma.esc_ok[i >> 5] |= ((p->enc_lut[i] >> 4) & 1u) << (i & 31);
+    ma.mark_bits = w.mark_bits;
+    ma.tile_marks = w.tile_marks;
+    ma.status = d_status;
+    e = p->chunk_size <= 256 ? launch_marks<1>(ma, s) : launch_marks<2>(ma, s);
+    if (e != cudaSuccess) return sz_record_cuda(e);
+    OffsetsArgs ta{};
+    ta.counts = w.tile_marks;
+    ta.n_counts = dtiles;
+    ta.offsets = w.tile_offsets;
+    ta.states = w.t_states;
+    ta.tile_counter = w.t_counter;
+    e = launch_scan(ta, s);
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
 
@@ -1083,7 +1506,7 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   a.m_ptr = in->d_n_escapes;
   a.codes = static_cast<const uint8_t*>(in->d_codes);
   a.sm = static_cast<const uint8_t*>(in->d_sm);
-  a.offsets = w.offsets;
+  a.offsets = marked ? w.tile_offsets : w.offsets;
   a.positions = in->d_positions;
   a.values = in->d_values;
   a.n = n;
@@ -1101,7 +1524,10 @@ int decode_impl(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
   a.sm_len = (n * sm_bits + 7) / 8;
   a.chunk = p->chunk_size;
   a.chunk_shift = (p->chunk_size & (p->chunk_size - 1)) == 0 ? __builtin_ctz(p->chunk_size) : -1;
-  const int posb = p->sentinel ? 0 : (p->abs32 ? 4 : (p->chunk_size <= 256 ? 1 : 2));
+  const int posb = p->sentinel ? 0
+                 : p->abs32  ? 4
+                 : marked    ? kPosMarked
+                             : (p->chunk_size <= 256 ? 1 : 2);
   switch (p->fmt) {
     case SZ_BF16: e = dec_cb<SZ_BF16>(posb, *p, a, s); break;
     case SZ_E5M2: e = dec_cb<SZ_E5M2>(posb, *p, a, s); break;

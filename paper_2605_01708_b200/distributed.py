@@ -9,12 +9,16 @@ pipelined prefill -> decode handoff.
   histogram on its shard (K1) and one all-reduce(sum) of the int64 bins
   equals ``merge_stats`` (calibration.py:88-96: histograms are additive);
   every rank then runs the same deterministic ``select_codebook``.
-* Handoff: GPU i encodes chunk-aligned pieces and ships the compressed
-  sections to GPU j with NCCL point-to-point (NVLink/NVSwitch); GPU j
-  decodes each piece as it lands.  Encode of piece k+1, transfer of piece k
-  and decode of piece k-1 overlap.  Per piece the wire carries a 2-word
-  header (elements, escapes) then the sections in serialization order
-  (codec.py:176-184): counts, codes, sign|mantissa, positions, values.
+* Handoff: GPU i encodes chunk-aligned pieces and ships them to GPU j with
+  NCCL point-to-point (NVLink/NVSwitch); GPU j decodes each piece as it
+  lands.  Encode of piece k+1, transfer of piece k and decode of piece k-1
+  overlap.  Each piece is ONE buffer (``FrameLayout``: N, M and the sections
+  in serialization order, codec.py:176-184) that the encoder writes in place
+  and the decoder reads in place, with M read on the device — one send per
+  piece and no host round trip inside the loop on either side.  Pieces whose
+  escapes overflow the frame's capacity are re-sent after the last piece as
+  spill frames sized for their M (one host sync per transfer, at the end).
+  The fused alternative without NCCL is peer.py.
 
 The codec itself is injected (``PieceCodec``) so the protocol is exercised by
 CPU/gloo tests with the oracle; the product binding is ``GpuPieceCodec``.
@@ -35,7 +39,8 @@ from .formats import ElementFormat
 
 __all__ = [
     "kv_shard_shape", "shard_range", "calibrate_sharded", "PieceCodec", "GpuPieceCodec",
-    "Sections", "HandoffSender", "HandoffReceiver", "send_raw", "recv_raw",
+    "FrameLayout", "default_frame_capacity", "HandoffSender", "HandoffReceiver", "send_raw",
+    "recv_raw",
 ]
 
 
@@ -81,111 +86,231 @@ def calibrate_sharded(local_counts: torch.Tensor, fmt: ElementFormat, code_bits:
 
 
 # ----------------------------------------------------------------- handoff
-@dataclass
-class Sections:
-    """One piece's compressed sections as flat byte tensors + counts."""
+_ALIGN = 256
 
-    n: int
-    m: int
-    counts: torch.Tensor      # uint8 view of u32 counts
-    codes: torch.Tensor
-    sm: torch.Tensor
-    positions: torch.Tensor   # uint8 view
-    values: torch.Tensor      # raw exponent bytes
 
-    def wire(self) -> list[torch.Tensor]:
-        return [t for t in (self.counts, self.codes, self.sm, self.positions, self.values)
-                if t.numel()]
+def _up(x: int) -> int:
+    return (x + _ALIGN - 1) // _ALIGN * _ALIGN
 
-    @property
-    def nbytes(self) -> int:
-        return sum(t.numel() for t in self.wire())
+
+class FrameLayout:
+    """One piece on the wire: a single contiguous buffer holding a 16-byte
+    header (N, M as little-endian u64) and the sections in serialization
+    order (codec.py:176-184) — counts, codes, sign|mantissa, positions,
+    values — at 256-byte aligned offsets, the escape sections sized for
+    ``capacity`` escapes.  The encoder writes straight into it (M included,
+    on the device) and the decoder reads it in place, so a piece costs one
+    NCCL send of ``wire_bytes`` and no host round trip on either side.
+    (The SPLZ container packs its sections back to back, so its codes and
+    sign|mantissa planes are not 16-byte aligned for the decoder's bulk
+    copies; ``container.frame_device`` produces it when a file is wanted.)
+    FP8 encoders also need a packed-values scratch, placed after the wire."""
+
+    def __init__(self, config: CodecConfig, n: int, capacity: int):
+        self.n, self.capacity = n, capacity
+        fmt = config.fmt
+        sizes = [("counts", 4 * config.n_chunks(n)),
+                 ("codes", packed_nbytes(n, config.code_bits)),
+                 ("sm", config.sm_nbytes(n)),
+                 ("positions", 0 if config.sentinel else capacity * config.position_nbytes),
+                 ("values", capacity)]
+        off = _ALIGN
+        self.off: dict[str, int] = {}
+        self.size: dict[str, int] = {}
+        for name, sz in sizes:
+            self.off[name], self.size[name] = off, sz
+            off = _up(off + sz)
+        self.wire_bytes = off
+        self.packed_off = off
+        self.total = _up(off + (packed_nbytes(capacity, fmt.exp_bits) if fmt.exp_bits != 8 else 0))
+
+    def view(self, frame: torch.Tensor, name: str) -> torch.Tensor:
+        o = self.off[name]
+        return frame[o:o + self.size[name]]
 
 
 class PieceCodec(Protocol):
-    """Codec seen by the handoff: ``slot`` (0/1) selects one of two buffer
-    sets so piece k+1 can be encoded/received while piece k is in flight."""
+    """Codec seen by the handoff.  ``slot`` (0/1) selects one of two frame
+    sets so piece k+1 is encoded / received while piece k is in flight.
+
+    Sender: ``encode_frame`` enqueues the encode of a piece into its slot's
+    frame and returns the wire tensor; ``overflowed`` (one host sync, after
+    the last piece) lists the pieces whose M exceeded the frame capacity;
+    ``spill_frame`` re-encodes such a piece into a frame sized for its M.
+    Receiver: ``recv_frame`` gives the buffer a piece lands in,
+    ``decode_frame`` enqueues its decode (M read from the frame header on
+    the device), ``finish`` checks every verdict once."""
 
     device: torch.device
 
-    def encode(self, words: torch.Tensor, slot: int) -> Sections: ...
+    def encode_frame(self, words: torch.Tensor, slot: int) -> torch.Tensor: ...
 
-    def empty_sections(self, n: int, m: int, slot: int) -> Sections: ...
+    def overflowed(self) -> list[tuple[int, int]]: ...
 
-    def decode_into(self, sec: Sections, out: torch.Tensor, slot: int) -> None: ...
+    def spill_frame(self, words: torch.Tensor, m: int) -> torch.Tensor: ...
 
-    def finish(self) -> None: ...
+    def recv_frame(self, n: int, slot: int, capacity: int | None = None) -> torch.Tensor: ...
+
+    def decode_frame(self, frame: torch.Tensor, n: int, out: torch.Tensor, slot: int,
+                     capacity: int | None = None) -> None: ...
+
+    def finish(self, redone: set[int] | None = None) -> None: ...
 
 
-def section_sizes(config: CodecConfig, n: int, m: int) -> tuple[int, int, int, int, int]:
-    return (4 * config.n_chunks(n), packed_nbytes(n, config.code_bits), config.sm_nbytes(n),
-            m * config.position_nbytes if not config.sentinel else 0, m)
+def default_frame_capacity(n: int) -> int:
+    """Escape capacity of a handoff frame: 1/32 of the piece (3.1% escapes;
+    realistic KV is 0.16-1.2%), so the frame is ~6% above the realistic
+    payload.  Pieces with more escapes take the spill path."""
+    return max(1, min(n, max(1024, n // 32)))
 
 
 class GpuPieceCodec:
-    """Product binding: the sm_100a kernels through the C ABI (DeviceCodec),
-    two engines per piece length (ping-pong), decode verdicts checked once at
-    the end so decode never stalls the receive loop."""
+    """Product binding: the sm_100a kernels through the C ABI, writing and
+    reading ``FrameLayout`` buffers.  Per (piece length, slot) one frame and
+    one workspace; the sender logs every piece's device M (an 8-byte device
+    copy) and reads them all once, after the last piece; the receiver keeps
+    one status word per piece and checks them all in ``finish``."""
 
     def __init__(self, config: CodecConfig, codebook: ExponentCodebook,
                  capacity: int | None = None):
+        from . import _native as N
+        from .codec import _config_params
+        self.N = N
+        self.lib = N.load_library()
         self.config, self.codebook, self.capacity = config, codebook, capacity
-        from . import _native as N
         self.device = N.device()
-        self._eng: dict[tuple[int, int], object] = {}
-        self._used: list = []
+        self.params = _config_params(config, codebook)
+        self._frames: dict[tuple, tuple[FrameLayout, torch.Tensor]] = {}
+        self._ws: dict[tuple, torch.Tensor] = {}
+        self._m_log: list[torch.Tensor] = []
+        self._piece_n: list[int] = []
+        self._status: list[tuple[int, bool, int, torch.Tensor]] = []  # (piece, spill, n, status)
 
-    def _engine(self, n: int, slot: int):
-        from .engine import DeviceCodec
-        key = (n, slot)
-        if key not in self._eng:
-            self._eng[key] = DeviceCodec(self.config, self.codebook, n, capacity=self.capacity,
-                                         device=self.device)
-        return self._eng[key]
+    def _cap(self, n: int, capacity: int | None) -> int:
+        if capacity is not None:
+            return max(1, min(n, capacity))
+        return max(1, min(n, self.capacity)) if self.capacity else default_frame_capacity(n)
 
-    def encode(self, words: torch.Tensor, slot: int) -> Sections:
-        eng = self._engine(words.numel(), slot)
-        m = eng.ensure_capacity(words)   # host learns M (sizes the escape sends)
-        b = eng.bufs
-        pos = b.positions[:m].view(torch.uint8) if b.positions is not None else \
-            torch.empty(0, dtype=torch.uint8, device=self.device)
-        return Sections(words.numel(), m, b.counts.view(torch.uint8), b.codes, b.sm, pos,
-                        b.values[:m])
+    def _frame(self, n: int, slot, capacity: int) -> tuple[FrameLayout, torch.Tensor]:
+        key = (n, slot, capacity)
+        if key not in self._frames:
+            lay = FrameLayout(self.config, n, capacity)
+            fr = torch.zeros(lay.total, dtype=torch.uint8, device=self.device)
+            fr[:8].view(torch.int64).fill_(n)
+            self._frames[key] = (lay, fr)
+        return self._frames[key]
 
-    def empty_sections(self, n: int, m: int, slot: int) -> Sections:
-        sizes = section_sizes(self.config, n, m)
-        ts = [torch.empty(sz, dtype=torch.uint8, device=self.device) for sz in sizes]
-        return Sections(n, m, *ts)
+    def _workspace(self, kind: str, n: int, m: int) -> torch.Tensor:
+        need = (self.lib.sz_encode_workspace_bytes(n, self.params) if kind == "enc"
+                else self.lib.sz_decode_workspace_bytes(n, m, self.params))
+        ws = self._ws.get((kind, n))
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self._ws[(kind, n)] = ws
+        return ws
 
-    def decode_into(self, sec: Sections, out: torch.Tensor, slot: int) -> None:
-        eng = self._engine(sec.n, slot)
-        cfg = self.config
-        counts = sec.counts.view(torch.uint32) if sec.counts.numel() else None
-        pos = sec.positions.view(cfg.position_torch_dtype) if sec.positions.numel() else None
-        src = eng.decode_struct(codes=sec.codes, sm=sec.sm, counts=counts, positions=pos,
-                                values=sec.values if sec.m else None, m=sec.m)
-        # each decode gets its own status word so verdicts survive until finish()
-        import torch as _t
-        from . import _native as N
-        status = _t.empty(N.STATUS_BYTES, dtype=_t.uint8, device=self.device)
-        N.check(eng.lib.sz_decode(src, eng.params, N.ptr(out), N.ptr(status), N.ptr(eng.dec_ws),
-                                  eng.dec_ws.numel(), N.stream_handle()), "decode")
-        self._used.append((status, sec))
+    def _encoded(self, lay: FrameLayout, fr: torch.Tensor):
+        N, cfg = self.N, self.config
+        s = N.SzEncoded()
+        s.d_codes = N.ptr(lay.view(fr, "codes"))
+        s.d_sm = N.ptr(lay.view(fr, "sm"))
+        s.d_counts = N.ptr(lay.view(fr, "counts")) if lay.size["counts"] else None
+        s.d_positions = N.ptr(lay.view(fr, "positions")) if lay.size["positions"] else None
+        s.d_values = N.ptr(lay.view(fr, "values"))
+        s.d_values_packed = (fr.data_ptr() + lay.packed_off) if cfg.fmt.exp_bits != 8 else None
+        s.d_n_escapes = fr.data_ptr() + 8
+        s.escape_capacity = lay.capacity
+        s.d_escape_base = None
+        return s
 
-    def finish(self) -> None:
-        from .codec import _raise_from_status, EncodedStreams
-        for status, sec in self._used:
-            raw = status.cpu().numpy()
-            if raw[:8 + 8 * 13].any():
-                es = EncodedStreams(sec.n, sec.m, sec.codes, sec.sm,
-                                    sec.counts.view(torch.uint32), sec.positions, sec.values,
-                                    self.codebook)
-                _raise_from_status(raw, es, self.config, self.codebook, sec.values)
-        self._used.clear()
+    def _encode_into(self, words: torch.Tensor, lay: FrameLayout, fr: torch.Tensor) -> None:
+        N = self.N
+        n = words.numel()
+        ws = self._workspace("enc", n, 0)
+        N.check(self.lib.sz_encode(N.ptr(words), n, self.params, self._encoded(lay, fr),
+                                   N.ptr(ws), ws.numel(), N.stream_handle()), "encode")
+
+    # ------------------------------------------------------------ sender
+    def encode_frame(self, words: torch.Tensor, slot: int) -> torch.Tensor:
+        n = words.numel()
+        lay, fr = self._frame(n, slot, self._cap(n, None))
+        self._encode_into(words, lay, fr)
+        self._m_log.append(fr[8:16].view(torch.int64).clone())   # device copy, no sync
+        self._piece_n.append(n)
+        return fr[:lay.wire_bytes]
+
+    def overflowed(self) -> list[tuple[int, int]]:
+        if not self._m_log:
+            return []
+        ms = torch.cat(self._m_log).cpu().tolist()              # the one host sync
+        out = [(k, int(m)) for k, (m, n) in enumerate(zip(ms, self._piece_n))
+               if m > self._cap(n, None)]
+        self._m_log.clear()
+        self._piece_n.clear()
+        return out
+
+    def spill_frame(self, words: torch.Tensor, m: int) -> torch.Tensor:
+        n = words.numel()
+        lay, fr = self._frame(n, "spill", max(1, m))
+        self._encode_into(words, lay, fr)
+        return fr[:lay.wire_bytes]
+
+    # ------------------------------------------------------------ receiver
+    def recv_frame(self, n: int, slot, capacity: int | None = None) -> torch.Tensor:
+        lay, fr = self._frame(n, ("rx", slot), self._cap(n, capacity))
+        return fr[:lay.wire_bytes]
+
+    def decode_frame(self, frame: torch.Tensor, n: int, out: torch.Tensor, slot, piece: int,
+                     capacity: int | None = None) -> None:
+        N, cfg = self.N, self.config
+        lay = FrameLayout(cfg, n, self._cap(n, capacity))
+        src = N.SzEncodedIn()
+        src.d_codes = N.ptr(lay.view(frame, "codes"))
+        src.d_sm = N.ptr(lay.view(frame, "sm"))
+        src.d_counts = N.ptr(lay.view(frame, "counts")) if lay.size["counts"] else None
+        src.d_positions = N.ptr(lay.view(frame, "positions")) if lay.size["positions"] else None
+        src.d_values = N.ptr(lay.view(frame, "values"))
+        src.n_elements = n
+        src.n_escapes = lay.capacity          # capacity; M comes from the header
+        src.n_counts = cfg.n_chunks(n) if cfg.chunked else 0
+        src.d_n_escapes = frame.data_ptr() + 8
+        ws = self._workspace("dec", n, lay.capacity)
+        status = torch.empty(N.STATUS_BYTES, dtype=torch.uint8, device=self.device)
+        N.check(self.lib.sz_decode(src, self.params, N.ptr(out), N.ptr(status), N.ptr(ws),
+                                   ws.numel(), N.stream_handle()), "decode")
+        self._status.append((piece, slot == "spill", n, status))
+
+    def finish(self, redone: set[int] | None = None) -> None:
+        """Check every piece's verdict (one host sync).  ``redone``: pieces
+        whose first decode was superseded by a spill frame (their first
+        verdict is the expected capacity flag)."""
+        from .codec import _status_view
+        from .errors import CorruptionError, NativeError
+        redone = redone or set()
+        if not self._status:
+            return
+        raws = torch.stack([st for *_, st in self._status]).cpu().numpy()
+        verdict = 8 + 8 * self.N.NUM_CHECKS
+        for (k, spill, n, _), raw in zip(self._status, raws):
+            if (k in redone and not spill) or not raw[:verdict].any():
+                continue
+            st, first = _status_view(raw)
+            if st.flags & (1 << self.N.DEC_CAPACITY):
+                raise NativeError(f"handoff piece {k}: escape count above the frame capacity "
+                                  "and no spill frame followed")
+            bad = [i for i, f in enumerate(first) if f is not None]
+            raise CorruptionError(f"handoff piece {k} ({n} elements) failed the decode checks "
+                                  f"{bad} (flags {st.flags:#x})")
+        self._status.clear()
 
 
 class HandoffSender:
-    """Sender rank: encode chunk-aligned pieces and ship them (NCCL P2P)."""
+    """Sender rank: encode chunk-aligned pieces into frames and ship each
+    with one NCCL send.  The host never waits on the device inside the
+    loop: a slot's next encode is ordered after its previous send on the
+    stream (``Work.wait`` is a stream wait under NCCL), and the pieces'
+    escape counts are read once at the end, when pieces that overflowed
+    their frame are re-sent as spill frames sized for their M."""
 
     def __init__(self, codec: PieceCodec, peer: int, piece: int, group=None):
         self.codec, self.peer, self.piece, self.group = codec, peer, piece, group
@@ -194,51 +319,69 @@ class HandoffSender:
         n = words.numel()
         pieces = -(-n // self.piece)
         dev = self.codec.device
-        dist.send(torch.tensor([n, pieces], dtype=torch.int64, device=dev), self.peer,
-                  group=self.group)
-        wire_bytes, escapes = 16, 0
-        inflight: list[tuple[list, torch.Tensor | None]] = [([], None), ([], None)]
+        dist.send(torch.tensor([n, pieces, self.piece], dtype=torch.int64, device=dev),
+                  self.peer, group=self.group)
+        wire_bytes = 24
+        inflight: list[list] = [[], []]
         for k in range(pieces):
             slot = k % 2
-            for r in inflight[slot][0]:   # buffers of piece k-2 must have left
+            for r in inflight[slot]:     # frame of piece k-2 must have left
                 r.wait()
-            sec = self.codec.encode(words[k * self.piece:(k + 1) * self.piece], slot)
-            h = torch.tensor([sec.n, sec.m], dtype=torch.int64, device=dev)
-            reqs = [dist.isend(h, self.peer, group=self.group)]
-            reqs += [dist.isend(t, self.peer, group=self.group) for t in sec.wire()]
-            inflight[slot] = (reqs, h)   # h kept alive until its send completes
-            wire_bytes += 16 + sec.nbytes
-            escapes += sec.m
-        for reqs, _ in inflight:
+            fr = self.codec.encode_frame(words[k * self.piece:(k + 1) * self.piece], slot)
+            inflight[slot] = [dist.isend(fr, self.peer, group=self.group)]
+            wire_bytes += fr.numel()
+        for reqs in inflight:
             for r in reqs:
                 r.wait()
-        return {"pieces": pieces, "wire_bytes": wire_bytes, "escapes": escapes}
+        spills = self.codec.overflowed()
+        lst = torch.tensor([[k, m] for k, m in spills] or [[-1, 0]], dtype=torch.int64,
+                           device=dev)
+        dist.send(torch.tensor([len(spills)], dtype=torch.int64, device=dev), self.peer,
+                  group=self.group)
+        wire_bytes += 8
+        if spills:
+            dist.send(lst, self.peer, group=self.group)
+            wire_bytes += lst.numel() * 8
+        for k, m in spills:
+            fr = self.codec.spill_frame(words[k * self.piece:(k + 1) * self.piece], m)
+            dist.send(fr, self.peer, group=self.group)
+            wire_bytes += fr.numel()
+        return {"pieces": pieces, "wire_bytes": wire_bytes, "spilled": len(spills)}
 
 
 class HandoffReceiver:
-    """Receiver rank: receive each piece and decode it as soon as it lands."""
+    """Receiver rank: each frame is received into its slot and decoded on
+    arrival (M read from the frame on the device); verdicts are checked
+    once, after the spill frames."""
 
     def __init__(self, codec: PieceCodec, peer: int, dtype: torch.dtype, group=None):
         self.codec, self.peer, self.dtype, self.group = codec, peer, dtype, group
 
     def recv(self) -> torch.Tensor:
         dev = self.codec.device
-        hdr = torch.empty(2, dtype=torch.int64, device=dev)
+        hdr = torch.empty(3, dtype=torch.int64, device=dev)
         dist.recv(hdr, self.peer, group=self.group)
-        n, pieces = (int(v) for v in hdr.cpu().tolist())
+        n, pieces, piece = (int(v) for v in hdr.cpu().tolist())
         out = torch.empty(n, dtype=self.dtype, device=dev)
-        lo = 0
         for k in range(pieces):
-            h = torch.empty(2, dtype=torch.int64, device=dev)
-            dist.recv(h, self.peer, group=self.group)
-            pn, pm = (int(v) for v in h.cpu().tolist())
-            sec = self.codec.empty_sections(pn, pm, k % 2)
-            reqs = [dist.irecv(t, self.peer, group=self.group) for t in sec.wire()]
-            for r in reqs:
-                r.wait()
-            self.codec.decode_into(sec, out[lo:lo + pn], k % 2)
-            lo += pn
-        self.codec.finish()
+            lo, hi = k * piece, min(n, (k + 1) * piece)
+            fr = self.codec.recv_frame(hi - lo, k % 2)
+            dist.irecv(fr, self.peer, group=self.group).wait()
+            self.codec.decode_frame(fr, hi - lo, out[lo:hi], k % 2, k)
+        cnt = torch.empty(1, dtype=torch.int64, device=dev)
+        dist.recv(cnt, self.peer, group=self.group)
+        c = int(cnt.item())
+        redone: set[int] = set()
+        if c:
+            lst = torch.empty((c, 2), dtype=torch.int64, device=dev)
+            dist.recv(lst, self.peer, group=self.group)
+            for k, m in lst.cpu().tolist():
+                lo, hi = k * piece, min(n, (k + 1) * piece)
+                fr = self.codec.recv_frame(hi - lo, "spill", capacity=m)
+                dist.recv(fr, self.peer, group=self.group)
+                self.codec.decode_frame(fr, hi - lo, out[lo:hi], "spill", k, capacity=m)
+                redone.add(k)
+        self.codec.finish(redone)
         return out
 
 

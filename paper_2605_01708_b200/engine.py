@@ -59,6 +59,11 @@ class DeviceCodec:
             self.capacity = m
             self.bufs = EncodeBuffers(self.n, self.config, m, self.device)
             self.encode(words)
+        # an escape-dense stream: room for the decoder's K3e path (escape
+        # bitmap + per-tile counts), which it then takes for this M
+        need = self.lib.sz_decode_workspace_bytes(self.n, m, self.params)
+        if need > self.dec_ws.numel():
+            self.dec_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return m
 
     def streams(self, m: int | None = None) -> EncodedStreams:

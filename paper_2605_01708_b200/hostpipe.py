@@ -225,7 +225,9 @@ def decode_host(streams: EncodedStreams, config: CodecConfig, codebook: Exponent
     cnt_d = [torch.empty(config.n_chunks(P), dtype=torch.uint32, device=dev) for _ in range(NBUF)]
     words_d = [torch.empty(P, dtype=fmt.torch_dtype, device=dev) for _ in range(NBUF)]
     status = torch.empty((npieces, N.STATUS_BYTES), dtype=torch.uint8, device=dev)
-    ws = [torch.empty(lib.sz_decode_workspace_bytes(P, 0, params), dtype=torch.uint8, device=dev)
+    # sized for any M: each piece takes the escape-dense (K3e) path when its
+    # declared M calls for it
+    ws = [torch.empty(lib.sz_decode_workspace_bytes(P, P, params), dtype=torch.uint8, device=dev)
           for _ in range(NBUF)]
 
     t_setup = time.perf_counter()

@@ -126,6 +126,28 @@ def handoff_bench(n: int, piece: int, reps: int, loopback: bool, rank: int = 0, 
             ok = torch.tensor([int(entry.get("bitexact", True))], device="cuda")
             dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
             entry["bitexact"] = bool(ok.item())
+        if not loopback and raw_baseline:
+            # NCCL variant: one framed buffer per piece (distributed.FrameLayout),
+            # M on the device, spill frames after the last piece
+            from paper_2605_01708_b200.distributed import (GpuPieceCodec, HandoffReceiver,
+                                                           HandoffSender)
+            pc = GpuPieceCodec(cfg, book)
+            got = {}
+
+            def frames():
+                if sender:
+                    got["stats"] = HandoffSender(pc, partner, piece, group=group).send(words)
+                else:
+                    got["out"] = HandoffReceiver(pc, partner, words.dtype, group=group).recv()
+            frames()
+            torch.cuda.synchronize()
+            entry["codec_nccl_frames_gbs"] = round(raw / (timed(frames) / 1e3) / 1e9, 1)
+            ok = torch.tensor([int(sender or torch.equal(got["out"], words))], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            entry["nccl_frames_bitexact"] = bool(ok.item())
+            if sender:
+                entry["nccl_frames_wire_bytes"] = got["stats"]["wire_bytes"]
+                entry["nccl_frames_spilled"] = got["stats"]["spilled"]
         m = int(sz.encode(sz.RawTensorStream(fmt, words[:1 << 24]), cfg).n_escapes)
         entry["escape_rate"] = round(m / (1 << 24), 5)
         res[tag] = entry

@@ -25,44 +25,82 @@ def _free_port() -> int:
 
 
 class OraclePieceCodec:
-    """CPU stand-in for GpuPieceCodec: same Sections on the wire."""
+    """CPU stand-in for GpuPieceCodec: the same FrameLayout buffers on the
+    wire (header N, M + sections at their offsets), capacity and spill
+    semantics included; sections from the oracle."""
 
     device = torch.device("cpu")
 
-    def __init__(self, config, book):
-        from paper_2605_01708_b200.codec import CodecConfig  # noqa: F401
-        self.config, self.book = config, tuple(book)
+    def __init__(self, config, book, capacity=None):
+        self.config, self.book, self.capacity = config, tuple(book), capacity
         self.p = O.Params(config.fmt.code, config.code_bits, config.sentinel,
                           config.chunk_size, config.abs32)
+        self.log, self.over = [], []
 
-    def encode(self, words, slot):
-        from paper_2605_01708_b200.distributed import Sections
+    def _cap(self, n, capacity):
+        from paper_2605_01708_b200.distributed import default_frame_capacity
+        if capacity is not None:
+            return max(1, min(n, capacity))
+        return max(1, min(n, self.capacity)) if self.capacity else default_frame_capacity(n)
+
+    def _frame(self, words, cap):
+        from paper_2605_01708_b200.distributed import FrameLayout
+        n = words.numel()
         sec = O.encode(words.numpy(), self.p, self.book)
-        t = lambda b: torch.from_numpy(np.frombuffer(bytes(b), dtype=np.uint8).copy())
-        return Sections(sec["n"], sec["m"], t(sec["chunk_counts"].astype("<u4").tobytes()),
-                        t(sec["packed_codes"]), t(sec["sign_mantissa"]),
-                        t(np.ascontiguousarray(sec["escape_positions"]).tobytes()),
-                        torch.from_numpy(sec["escape_values"].copy()))
+        lay = FrameLayout(self.config, n, cap)
+        fr = torch.zeros(lay.wire_bytes, dtype=torch.uint8)
+        fr[:16].view(torch.int64)[:] = torch.tensor([n, sec["m"]])
+        k = min(sec["m"], cap)
+        put = lambda name, b: lay.view(fr, name)[:len(b)].copy_(
+            torch.from_numpy(np.frombuffer(bytes(b), dtype=np.uint8).copy()))
+        put("counts", sec["chunk_counts"].astype("<u4").tobytes())
+        put("codes", sec["packed_codes"])
+        put("sm", sec["sign_mantissa"])
+        put("positions", np.ascontiguousarray(sec["escape_positions"][:k]).tobytes())
+        put("values", sec["escape_values"][:k].tobytes())
+        return fr, sec["m"]
 
-    def empty_sections(self, n, m, slot):
-        from paper_2605_01708_b200.distributed import Sections, section_sizes
-        sizes = section_sizes(self.config, n, m)
-        return Sections(n, m, *[torch.empty(s, dtype=torch.uint8) for s in sizes])
+    def encode_frame(self, words, slot):
+        fr, m = self._frame(words, self._cap(words.numel(), None))
+        self.log.append((words.numel(), m))
+        return fr
 
-    def decode_into(self, sec, out, slot):
+    def overflowed(self):
+        out = [(k, m) for k, (n, m) in enumerate(self.log) if m > self._cap(n, None)]
+        self.log = []
+        return out
+
+    def spill_frame(self, words, m):
+        return self._frame(words, max(1, m))[0]
+
+    def recv_frame(self, n, slot, capacity=None):
+        from paper_2605_01708_b200.distributed import FrameLayout
+        return torch.empty(FrameLayout(self.config, n, self._cap(n, capacity)).wire_bytes,
+                           dtype=torch.uint8)
+
+    def decode_frame(self, frame, n, out, slot, piece, capacity=None):
+        from paper_2605_01708_b200.distributed import FrameLayout
+        cap = self._cap(n, capacity)
+        lay = FrameLayout(self.config, n, cap)
+        hn, m = (int(v) for v in frame[:16].view(torch.int64))
+        assert hn == n
+        if m > cap:
+            self.over.append((piece, slot == "spill"))
+            return
         pos_dt = self.config.position_np_dtype
-        d = {"n": sec.n, "m": sec.m,
-             "chunk_counts": sec.counts.numpy().view(np.uint32),
-             "packed_codes": sec.codes.numpy().tobytes(),
-             "sign_mantissa": sec.sm.numpy().tobytes(),
-             "escape_positions": sec.positions.numpy().view(pos_dt),
-             "escape_values": sec.values.numpy()}
-        out.copy_(torch.from_numpy(O.decode(d, self.p, self.book).astype(np.int32)).to(out.dtype)
-                  if out.dtype != torch.uint16 else
-                  torch.from_numpy(O.decode(d, self.p, self.book)))
+        d = {"n": n, "m": m,
+             "chunk_counts": lay.view(frame, "counts").numpy().view(np.uint32),
+             "packed_codes": lay.view(frame, "codes").numpy().tobytes(),
+             "sign_mantissa": lay.view(frame, "sm").numpy().tobytes(),
+             "escape_positions": lay.view(frame, "positions").numpy().view(pos_dt)[:m],
+             "escape_values": lay.view(frame, "values").numpy()[:m]}
+        out.copy_(torch.from_numpy(O.decode(d, self.p, self.book)))
 
-    def finish(self):
-        pass
+    def finish(self, redone=None):
+        redone = redone or set()
+        left = [k for k, spill in self.over if spill or k not in redone]
+        assert not left, f"pieces {left} overflowed without a spill frame"
+        self.over = []
 
 
 def _worker(rank, world, port, q, rate, piece):
@@ -85,8 +123,14 @@ def _worker(rank, world, port, q, rate, piece):
         codec = OraclePieceCodec(cfg, book.entries)
         if rank == 0:
             stats = HandoffSender(codec, 1, piece).send(torch.from_numpy(words.copy()))
-            ref = O.encode(words, O.Params(0), book.entries)
-            q.put(("sender", stats["escapes"] == ref["m"], stats["pieces"]))
+            # pieces over the frame capacity (1/32 of the piece, >= 1024)
+            # travel as spill frames
+            from paper_2605_01708_b200.distributed import default_frame_capacity
+            want = 0
+            for lo in range(0, n, piece):
+                w = words[lo:lo + piece]
+                want += O.encode(w, O.Params(0), book.entries)["m"] > default_frame_capacity(w.size)
+            q.put(("sender", stats["spilled"] == want, stats["pieces"]))
         else:
             out = HandoffReceiver(codec, 0, torch.uint16).recv()
             q.put(("receiver", bool(np.array_equal(out.numpy(), words)), n))

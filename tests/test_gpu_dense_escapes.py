@@ -3,7 +3,10 @@ outside the book; the handoff tests use 7.89%; all-escape chunks exist in
 the reference's own matrix): the encoder's staged-record path (K2a writers,
 K2b moves) and the decoder's K3e scatter + bitmap staging, checked against
 the CPU oracle section for section, bit for bit, and verdict for verdict on
-corrupted streams (exception class and chunk, codec.py:404-536)."""
+corrupted streams (exception class and chunk, codec.py:404-536).  Every
+case runs the decoder both ways (SZ_DEC_MARKED forces the path): the K3e
+pre-pass (escape bitmap + tile counts, sentinel-style staging) and the
+stagers' own walk over positions (the path realistic rates take)."""
 
 from __future__ import annotations
 
@@ -43,7 +46,8 @@ CASES = [  # fmt, chunk, rate, code bits, n
     (0, 1024, 0.0789, 4, 5 * 8192 + 333), (0, 1024, 0.0689, 3, 4 * 8192),
     (0, 64, 0.2, 4, 3 * 8192 + 17), (0, 256, 0.03, 3, 6 * 8192 + 1),
     (0, 8192, 0.5, 4, 2 * 8192 + 4095), (0, 4096, 0.009, 4, 8 * 8192 + 9),
-    (0, 1000, 0.07, 4, 3 * 8192 + 5),          # chunk not dividing the tile: stager path
+    (0, 1000, 0.07, 4, 3 * 8192 + 5),          # chunk not dividing the tile
+    (0, 48, 0.1, 3, 3 * 8192 + 100),           # chunk not a power of two, < a bitmap window word run
     (0, 16384, 0.07, 4, 5 * 8192),             # chunk larger than the decode tile
     (1, 1024, 0.0789, 4, 3 * 16384 + 77), (1, 1024, 0.0689, 3, 4 * 16384),
     (1, 16384, 0.3, 4, 2 * 16384 + 1), (1, 128, 0.05, 3, 3 * 16384 + 3),
@@ -53,8 +57,14 @@ CASES = [  # fmt, chunk, rate, code bits, n
 ]
 
 
+@pytest.fixture(params=["0", "1"], ids=["stager", "k3e"])
+def dec_path(request, monkeypatch):
+    monkeypatch.setenv("SZ_DEC_MARKED", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("fmt_id,chunk,rate,cb,n", CASES)
-def test_dense_roundtrip_matches_oracle(fmt_id, chunk, rate, cb, n):
+def test_dense_roundtrip_matches_oracle(fmt_id, chunk, rate, cb, n, dec_path):
     m = sz()
     words, book = dense_case(fmt_id, n, rate, cb, 1000 + n % 97)
     fmt, cfg = config(fmt_id, cb, chunk, book)
@@ -65,7 +75,8 @@ def test_dense_roundtrip_matches_oracle(fmt_id, chunk, rate, cb, n):
     assert [b for _, b in enc.section_bytes()] == O.section_bytes(ref)
     dec = m.decode(enc, cfg, enc.codebook)
     assert torch.equal(dec.words, stream.words)
-    # the engine path: M stays on the device, K3e runs and each tile decides
+    # the engine path: M stays on the device (workspace sized for K3e by
+    # ensure_capacity)
     from paper_2605_01708_b200.engine import DeviceCodec
     eng = DeviceCodec(cfg, enc.codebook, n)
     eng.ensure_capacity(stream.words)
@@ -109,7 +120,7 @@ def _mutations(sec, chunk, rng):
     (0, 1024, 0.0789, 4, 5 * 8192 + 333), (0, 256, 0.05, 3, 3 * 8192 + 7),
     (1, 1024, 0.0689, 3, 3 * 16384 + 77),
 ])
-def test_dense_corruption_verdicts_match_oracle(fmt_id, chunk, rate, cb, n):
+def test_dense_corruption_verdicts_match_oracle(fmt_id, chunk, rate, cb, n, dec_path):
     m = sz()
     words, book = dense_case(fmt_id, n, rate, cb, 77 + n % 31)
     fmt, cfg = config(fmt_id, cb, chunk, book)

@@ -57,6 +57,22 @@ def test_encode_decode_matches_reference(cid, device_api):
 
 
 @pytest.mark.parametrize("cid", golden_case_ids())
+def test_decode_k3e_path_matches_reference(cid, monkeypatch):
+    # every chunk-relative golden case (chunk >= 32) decoded through the
+    # escape-dense pre-pass path (K3e bitmap + sentinel-style staging),
+    # whatever its escape rate; other modes ignore the switch
+    monkeypatch.setenv("SZ_DEC_MARKED", "1")
+    m = sz()
+    g = golden()
+    case = g.case(cid)
+    words = g.arr(cid, "words")
+    fmt, cfg = make_config(case)
+    enc = m.encode(m.RawTensorStream(fmt, torch.from_numpy(words.copy()).cuda()), cfg)
+    dec = m.decode(enc, cfg, enc.codebook)
+    assert np.array_equal(dec.words.cpu().numpy(), words)
+
+
+@pytest.mark.parametrize("cid", golden_case_ids())
 def test_histogram_matches_reference(cid):
     m = sz()
     g = golden()
@@ -67,8 +83,11 @@ def test_histogram_matches_reference(cid):
     assert m.entropy_bits(stats) == pytest.approx(case["entropy"], abs=1e-12)
 
 
+@pytest.mark.parametrize("path", ["auto", "k3e"])
 @pytest.mark.parametrize("verdict", golden().corruptions, ids=lambda v: v["id"])
-def test_corruption_verdicts_match_reference(verdict):
+def test_corruption_verdicts_match_reference(verdict, path, monkeypatch):
+    if path == "k3e":
+        monkeypatch.setenv("SZ_DEC_MARKED", "1")
     m = sz()
     g = golden()
     base, words = g.corruption_base(verdict)
@@ -283,25 +302,37 @@ def test_host_pipeline_matches_oracle(host_kind, monkeypatch):
         assert exc.value.chunk == oexc.value.chunk
 
 
+@pytest.mark.parametrize("fmt_id", [0, 1])
 @pytest.mark.parametrize("rate", [0.0016, 0.0789, 0.5])
-def test_gpu_piece_codec_loopback(rate):
-    """The handoff's product binding (GpuPieceCodec) on one GPU: encode
-    pieces, copy the wire tensors as NCCL would, decode into place."""
+def test_gpu_piece_codec_loopback(rate, fmt_id):
+    """The handoff's product binding (GpuPieceCodec) on one GPU: encode each
+    piece into its frame (M on the device), copy the frame as the NCCL send
+    would, decode it in place; pieces over the frame capacity go through the
+    spill path exactly as HandoffSender/Receiver run it."""
     m = sz()
     from paper_2605_01708_b200.distributed import GpuPieceCodec
     n, piece = 300_000, 1 << 16
-    words = O.exact_stream(0, n, rate, 3, O.BF16_BOOK, O.BF16_ESC)
-    book = m.ExponentCodebook(m.ElementFormat.BF16, tuple(e for e, _ in O.BF16_BOOK), 4,
-                              m.CodebookMode.TOPK_EXPLICIT)
-    cfg = m.CodecConfig(m.ElementFormat.BF16, codebook=book)
+    bk, esc = (O.BF16_BOOK, O.BF16_ESC) if fmt_id == 0 else (O.E5M2_BOOK, O.E5M2_ESC)
+    fmt = list(m.ElementFormat)[fmt_id]
+    words = O.exact_stream(fmt_id, n, rate, 3, bk, esc)
+    book = m.ExponentCodebook(fmt, tuple(e for e, _ in bk), 4, m.CodebookMode.TOPK_EXPLICIT)
+    cfg = m.CodecConfig(fmt, codebook=book)
     tx, rx = GpuPieceCodec(cfg, book), GpuPieceCodec(cfg, book)
     src = torch.from_numpy(words).cuda()
     out = torch.empty_like(src)
-    for k, lo in enumerate(range(0, n, piece)):
-        sec = tx.encode(src[lo:lo + piece], k % 2)
-        dst = rx.empty_sections(sec.n, sec.m, k % 2)
-        for a, b in zip(dst.wire(), sec.wire()):
-            a.copy_(b)
-        rx.decode_into(dst, out[lo:lo + piece], k % 2)
-    rx.finish()
+    bounds = [(lo, min(n, lo + piece)) for lo in range(0, n, piece)]
+    for k, (lo, hi) in enumerate(bounds):
+        fr = tx.encode_frame(src[lo:hi], k % 2)
+        dst = rx.recv_frame(hi - lo, k % 2)
+        dst.copy_(fr)
+        rx.decode_frame(dst, hi - lo, out[lo:hi], k % 2, k)
+    spills = tx.overflowed()
+    assert bool(spills) == (rate > 1 / 32)
+    for k, mk in spills:
+        lo, hi = bounds[k]
+        fr = tx.spill_frame(src[lo:hi], mk)
+        dst = rx.recv_frame(hi - lo, "spill", capacity=mk)
+        dst.copy_(fr)
+        rx.decode_frame(dst, hi - lo, out[lo:hi], "spill", k, capacity=mk)
+    rx.finish({k for k, _ in spills})
     assert torch.equal(out, src)

@@ -52,11 +52,11 @@ def test_peer_loopback_roundtrip(fmt_name, rate):
     rcv.release()
 
 
-def _ipc_worker(rank, world, port, fmt_name, q):
+def _ipc_worker(rank, world, port, fmt_name, q, cross=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(rank if cross else 0)
     try:
         from paper_2605_01708_b200 import peer
         m, fmt, words, book, cfg = setup(fmt_name, 3 * (1 << 20) + 2048, 0.0016)
@@ -90,13 +90,62 @@ def _ipc_worker(rank, world, port, fmt_name, q):
         dist.destroy_process_group()
 
 
+two_gpus = pytest.mark.skipif(torch.cuda.device_count() < 2,
+                              reason="needs two GPUs (cuda:0 -> cuda:1 over NVLink)")
+
+
+@pytest.mark.parametrize("cross", [False, pytest.param(True, marks=two_gpus)],
+                         ids=["same-gpu", "cuda0-to-cuda1"])
 @pytest.mark.parametrize("fmt_name", ["bf16", "e5m2"])
-def test_peer_two_processes_ipc(fmt_name):
+def test_peer_two_processes_ipc(fmt_name, cross):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + (os.getpid() % 200)
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, fmt_name, q)) for r in range(2)]
+    port = 29600 + (os.getpid() % 200) + (7 if cross else 0)
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, fmt_name, q, cross))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = dict(q.get(timeout=5) for _ in range(2))
+    assert res == {0: True, 1: True}
+    assert [p.exitcode for p in procs] == [0, 0]
+
+
+def _nccl_frames_worker(rank, world, port, fmt_name, rate, q):
+    """HandoffSender/Receiver over NCCL with GpuPieceCodec frames, rank r on
+    cuda:r: one framed buffer per piece, spill frames for overflowing pieces."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        from paper_2605_01708_b200.distributed import (GpuPieceCodec, HandoffReceiver,
+                                                       HandoffSender)
+        m, fmt, words, book, cfg = setup(fmt_name, 3 * (1 << 20) + 4096, rate)
+        codec = GpuPieceCodec(cfg, book)
+        if rank == 0:
+            st = HandoffSender(codec, 1, 1 << 20).send(words)
+            ok = (st["spilled"] > 0) == (rate > 1 / 32)
+        else:
+            out = HandoffReceiver(codec, 0, words.dtype).recv()
+            ok = bool(torch.equal(out, words))
+        torch.cuda.synchronize()
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@two_gpus
+@pytest.mark.parametrize("fmt_name,rate", [("bf16", 0.0016), ("bf16", 0.0789), ("e5m2", 0.0016)])
+def test_nccl_frame_handoff_two_gpus(fmt_name, rate):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29900 + (os.getpid() % 90)
+    procs = [ctx.Process(target=_nccl_frames_worker, args=(r, 2, port, fmt_name, rate, q))
+             for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

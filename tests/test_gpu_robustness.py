@@ -46,9 +46,14 @@ def _want(v):
     return ("raise", v["raised"], v["section"], v["chunk"], v["msg"])
 
 
+@pytest.mark.parametrize("path", ["auto", "k3e"])
 @pytest.mark.parametrize("where", ["host", "device"])
 @pytest.mark.parametrize("bid", _bases())
-def test_decode_container_verdicts_match_reference(bid, where):
+def test_decode_container_verdicts_match_reference(bid, where, path, monkeypatch):
+    # "k3e": every chunk-relative decode (chunk >= 32) forced through the
+    # escape-dense pre-pass path, whatever its escape rate
+    if path == "k3e":
+        monkeypatch.setenv("SZ_DEC_MARKED", "1")
     from paper_2605_01708_b200.container import decode_container
     r = robust()
     bad = []
