@@ -65,13 +65,20 @@ constexpr uint32_t kTileCap = kEncSlots * kEpv<FMT> / 8 < kEscValCap<FMT>
                                   ? kEncSlots * kEpv<FMT> / 8 : kEscValCap<FMT>;
 // Writer warps: the escape records' placement is a per-tile serial chain
 // per writer, so escape-dense BF16 tiles want many (7: 16 + 1 + 7 = 24 warps
-// at 80 registers); the FP8 dense warps are issue-bound and need the
-// registers (3: 20 warps at 96).  Warp counts stay multiples of 4 so the
-// register file splits evenly.
-template <int FMT>
-constexpr int kWriterWarps = FMT == SZ_BF16 ? 7 : 3;
-template <int FMT>
-constexpr int kEncThreads = kEncDense + 32 * (1 + kWriterWarps<FMT>);
+// at 80 registers); the FP8 dense warps of realistic books are issue-bound
+// and need the registers (3: 20 warps at 96).  E5M2 with 3-bit codes (top-8
+// books: ~7% escapes, twice BF16's per tile) was writer-bound with 3 (per-role
+// cycle counters: writers busy 95% of the kernel, the producer waiting on
+// their scan slots): 7 writers at 80 registers, 7 scan slots so the shared
+// memory fits — 1045 -> 1183 GB/s; E4M3 3-bit books are sparse and lost 5%
+// with 7, so they keep 3.  Warp counts stay multiples of 4 so the register
+// file splits evenly.
+template <int FMT, int CB>
+constexpr int kWriterWarps = FMT == SZ_BF16 ? 7 : (FMT == SZ_E5M2 && CB == 3 ? 7 : 3);
+template <int FMT, int CB>
+constexpr int kScanSlots = FMT == SZ_E5M2 && CB == 3 ? 7 : kEncScanSlots;
+template <int FMT, int CB>
+constexpr int kEncThreads = kEncDense + 32 * (1 + kWriterWarps<FMT, CB>);
 constexpr int kProducerWarp = kEncDenseWarps;           // warp 16
 constexpr int kWriterWarp0 = kEncDenseWarps + 1;        // warps 17..
 
@@ -111,24 +118,25 @@ struct EncodeArgs {
   int32_t seg_tmap;
 };
 
-template <int FMT>
+template <int FMT, int CB>
 struct EncSmem {
+  static constexpr int Q = kScanSlots<FMT, CB>;
   // 1024-aligned: the 128B-swizzle pattern of tensor TMA is a function of
   // shared-address bits 7-9
   alignas(1024) uint8_t in[kEncInStages][kEncTileBytes];
-  uint32_t fmask[kEncScanSlots][kEncSlots];  // at fsw(slot)
+  uint32_t fmask[Q][kEncSlots];  // at fsw(slot)
   // the tile's escape records, (tile-local element index, raw exponent), in
   // arbitrary order (one shared atomic per slot with escapes); the writer
   // derives each one's rank from fmask
-  uint16_t esc_idx[kEncScanSlots][kEscValCap<FMT>];
-  uint8_t esc_val[kEncScanSlots][kEscValCap<FMT>];
-  uint32_t esc_n[kEncScanSlots];
-  uint16_t slot_pref[kWriterWarps<FMT>][kEncSlots];  // per-slot exclusive escape prefix, at fsw(slot)
-  uint64_t meta[kEncScanSlots];      // tile id (~0 = end of work)
+  uint16_t esc_idx[Q][kEscValCap<FMT>];
+  uint8_t esc_val[Q][kEscValCap<FMT>];
+  uint32_t esc_n[Q];
+  uint16_t slot_pref[kWriterWarps<FMT, CB>][kEncSlots];  // per-slot exclusive escape prefix, at fsw(slot)
+  uint64_t meta[Q];      // tile id (~0 = end of work)
   uint64_t full[kEncInStages];       // producer -> dense (TMA bytes)
   uint64_t in_empty[kEncInStages];   // dense -> producer
-  uint64_t computed[kEncScanSlots];  // dense -> writer
-  uint64_t scan_empty[kEncScanSlots];// writer -> producer
+  uint64_t computed[Q];  // dense -> writer
+  uint64_t scan_empty[Q];// writer -> producer
 };
 
 // Shared-memory index of a slot's escape mask (and slot prefix).  Dense warps
@@ -363,7 +371,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 template <int FMT, int CB, int POSB>
-__global__ void __launch_bounds__(kEncThreads<FMT>, 1)
+__global__ void __launch_bounds__(kEncThreads<FMT, CB>, 1)
     encode_tiles(const __grid_constant__ sz_params p, const EncodeArgs a,
                  const __grid_constant__ CUtensorMap tmap) {
   constexpr int EPV = kEpv<FMT>;
@@ -373,10 +381,11 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
   constexpr int CBYTES = EPV * CB / 8;
   constexpr int SBYTES = EPV * SMB / 8;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  constexpr int NW = kWriterWarps<FMT>;
-  constexpr int NT = kEncThreads<FMT>;
+  constexpr int NW = kWriterWarps<FMT, CB>;
+  constexpr int NT = kEncThreads<FMT, CB>;
+  constexpr int QS = kScanSlots<FMT, CB>;
   constexpr int VCAP = kEscValCap<FMT>;
-  EncSmem<FMT>& S = *reinterpret_cast<EncSmem<FMT>*>(
+  EncSmem<FMT, CB>& S = *reinterpret_cast<EncSmem<FMT, CB>*>(
       smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -405,7 +414,7 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
       mbar_init(&S.full[s], 1);
       mbar_init(&S.in_empty[s], kEncDense);
     }
-    for (int q = 0; q < kEncScanSlots; ++q) {
+    for (int q = 0; q < QS; ++q) {
       mbar_init(&S.computed[q], kEncDense);
       mbar_init(&S.scan_empty[q], 32);  // every writer lane arrives
       S.esc_n[q] = 0;
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
       uint64_t next = ahead ? atomicAdd(a.tile_counter, 1ull) : 0;
       for (uint32_t it = 0;; ++it) {
         const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
-        const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
+        const uint32_t q = it % QS, qph = (it / QS) & 1;
         uint64_t seg_first = 0;
         if (ahead && next < a.num_tiles)
           seg_first = __ldg(a.seg_addrs + ((next * TILE * WB) >> a.seg_shift));
@@ -448,7 +457,7 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
           // writer residue class); the dense warps relay them (computed)
           S.meta[q] = ~0ull;
           for (uint32_t k = 1; k < NW; ++k) {
-            const uint32_t qk = (it + k) % kEncScanSlots, pk = ((it + k) / kEncScanSlots) & 1;
+            const uint32_t qk = (it + k) % QS, pk = ((it + k) / QS) & 1;
             mbar_wait(&S.scan_empty[qk], pk ^ 1);
             S.meta[qk] = ~0ull;
           }
@@ -512,7 +521,7 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
     long long t_wait = 0, t_work = 0;
     for (uint32_t it = 0;; ++it) {
       const uint32_t s = it % kEncInStages, sph = (it / kEncInStages) & 1;
-      const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
+      const uint32_t q = it % QS, qph = (it / QS) & 1;
       const long long c0 = SZ_CLOCK();
       mbar_wait(&S.full[s], sph);
       // direct ordering after the writer's release of this scan slot (also
@@ -523,7 +532,7 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
       const uint64_t tile = S.meta[q];
       if (tile == ~0ull) {
         for (uint32_t k = 0; k < NW; ++k)
-          mbar_arrive(&S.computed[(it + k) % kEncScanSlots]);
+          mbar_arrive(&S.computed[(it + k) % QS]);
         break;
       }
       const uint64_t tile_e0 = tile * TILE;
@@ -637,7 +646,7 @@ __global__ void __launch_bounds__(kEncThreads<FMT>, 1)
   const uint32_t key = fsw_key(lane);  // this lane's slots: lane*SPL + (j ^ key)
   long long t_wait = 0, t_work = 0;
   for (uint32_t it = ww;; it += NW) {
-    const uint32_t q = it % kEncScanSlots, qph = (it / kEncScanSlots) & 1;
+    const uint32_t q = it % QS, qph = (it / QS) & 1;
     const long long c0 = SZ_CLOCK();
     mbar_wait(&S.computed[q], qph);
     const long long c1 = SZ_CLOCK();
@@ -1272,13 +1281,13 @@ template <int FMT, int CB, int POSB>
 cudaError_t launch_encode(const sz_params& p, const EncodeArgs& a, const GatherArgs& g,
                           const CUtensorMap& tm, cudaStream_t s) {
   auto kern = encode_tiles<FMT, CB, POSB>;
-  const int smem = static_cast<int>(sizeof(EncSmem<FMT>)) + 1024;  // + alignment slack
-  const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kEncThreads<FMT>);
+  const int smem = static_cast<int>(sizeof(EncSmem<FMT, CB>)) + 1024;  // + alignment slack
+  const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kEncThreads<FMT, CB>);
   if (ks.err != cudaSuccess) return ks.err;
   cudaError_t e;
   const uint64_t want = static_cast<uint64_t>(ks.sms);
   const unsigned grid = static_cast<unsigned>(a.num_tiles < want ? a.num_tiles : want);
-  e = launch_pdl(kern, dim3(grid), dim3(kEncThreads<FMT>), smem, s, p, a, tm);
+  e = launch_pdl(kern, dim3(grid), dim3(kEncThreads<FMT, CB>), smem, s, p, a, tm);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   {
