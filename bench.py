@@ -445,7 +445,7 @@ def run_ours(args) -> None:
 
 def handoff_leg(rank: int, world: int, raw_baseline: bool = True, n: int = 1 << 30) -> dict:
     """Config 5 at N >= 2: pairs (2i -> 2i+1) hand 2 GiB of BF16 KV over in
-    64 MiB pieces — raw NCCL P2P vs the fused encode -> peer-store -> decode
+    256 MiB pieces — raw NCCL P2P vs the fused encode -> peer-store -> decode
     link (peer.py) — for realistic and escape-heavy exponent statistics.
     Reported beside the headline; never allowed to take the run down."""
     import datetime
@@ -455,7 +455,7 @@ def handoff_leg(rank: int, world: int, raw_baseline: bool = True, n: int = 1 << 
     try:
         from bench_handoff import handoff_bench
         gloo = dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=120))
-        res = handoff_bench(n, min(1 << 25, n), 3, False, rank, world, obj_group=gloo,
+        res = handoff_bench(n, min(1 << 27, n), 3, False, rank, world, obj_group=gloo,
                             timeout_s=20.0, raw_baseline=raw_baseline)
         res["pairs"] = world // 2
         res["unit"] = "GB/s of BF16 KV per pair (raw bytes / max device time over ranks)"

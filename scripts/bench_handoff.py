@@ -158,7 +158,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--loopback", action="store_true")
     ap.add_argument("--elems", type=int, default=1 << 30)       # 2 GiB of BF16 per pair
-    ap.add_argument("--piece", type=int, default=1 << 25)       # 64 MiB pieces
+    ap.add_argument("--piece", type=int, default=1 << 27)       # 256 MiB pieces
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the multi-process path with every rank on one GPU "
