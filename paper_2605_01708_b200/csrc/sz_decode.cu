@@ -1084,27 +1084,30 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         }
         uint32_t bm = S.bitmap[s][slot];
         const uint32_t bm0 = bm;
-        const uint32_t first = kGroupMerge && bm ? S.slot_first[s][slot] : 0u;
-        if (kGroupMerge && bm && first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
-          // group-wise PRMT merge of the placed exponent fields (bits 2-6)
-          const uint32_t vbase = smem_addr(S.vals[s]);
-          uint32_t r = first, nd_any = 0;
+        if constexpr (kGroupMerge) {
+          // group-wise PRMT merge of the placed exponent fields (bits 2-6),
+          // branch-free: a group without escapes merges with the identity
+          // selector (the slot's escape-free groups cost a few instructions
+          // instead of a divergent branch per group)
+          const uint32_t sf = S.slot_first[s][slot];
+          const uint32_t first = bm ? sf : 0u;
+          if (first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
+            const uint32_t vbase = smem_addr(S.vals[s]);
+            uint32_t r = first, nd_el = 0xFFu;
 #pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t mg = (bm >> (4 * g)) & 15u;
-            if (mg) {
+            for (int g = 0; g < G; ++g) {
+              const uint32_t mg = (bm >> (4 * g)) & 15u;
               uint32_t nd;
               const uint32_t t = merge_group(ow[g] >> 2 & 0x1F1F1F1Fu, mg, r, vbase, sel_base,
                                              d0 * 0x01010101u, &nd);
               ow[g] = (ow[g] & 0x83838383u) | ((t << 2) & 0x7C7C7C7Cu);
-              if (!SENT && nd && !nd_any) {
-                record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + 4 * g + (__ffs(nd) - 1) / 8);
-                nd_any = 1;
-              }
+              if (!SENT) nd_el = min(nd_el, nd ? 4u * g + (__ffs(nd) - 1) / 8 : 0xFFu);
               r += __popc(mg);
             }
+            if (!SENT && nd_el != 0xFFu)
+              record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + nd_el);
+            bm = 0;
           }
-          bm = 0;
         }
         while (bm) {  // rare: overwrite escaped exponent fields (bits 2-6 of the byte)
           const int j = __ffs(bm) - 1;
@@ -1160,26 +1163,27 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       if constexpr (EPV == 32) bm = S.bitmap[s][slot];
       else bm = (S.bitmap[s][slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
       const uint32_t bm0 = bm;
-      const uint32_t first = kGroupMerge && bm ? S.slot_first[s][slot] : 0u;
-      if (kGroupMerge && bm && first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
+      if constexpr (kGroupMerge) {
         // escaped exponents merged group by group (merge_group): no loop
-        // over the escapes, so escape-dense slots do not serialise the warp
-        const uint32_t vbase = smem_addr(S.vals[s]);
-        uint32_t r = first, nd_any = 0;
+        // over the escapes, so escape-dense slots do not serialise the warp;
+        // branch-free (escape-free groups merge with the identity selector)
+        const uint32_t sf = S.slot_first[s][slot];
+        const uint32_t first = bm ? sf : 0u;
+        if (first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
+          const uint32_t vbase = smem_addr(S.vals[s]);
+          uint32_t r = first, nd_el = 0xFFu;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const uint32_t mg = (bm >> (4 * g)) & 15u;
-          if (mg) {
+          for (int g = 0; g < G; ++g) {
+            const uint32_t mg = (bm >> (4 * g)) & 15u;
             uint32_t nd;
             eg[g] = merge_group(eg[g], mg, r, vbase, sel_base, d0 * 0x01010101u, &nd);
-            if (!SENT && nd && !nd_any) {
-              record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + 4 * g + (__ffs(nd) - 1) / 8);
-              nd_any = 1;
-            }
+            if (!SENT) nd_el = min(nd_el, nd ? 4u * g + (__ffs(nd) - 1) / 8 : 0xFFu);
             r += __popc(mg);
           }
+          if (!SENT && nd_el != 0xFFu)
+            record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + nd_el);
+          bm = 0;
         }
-        bm = 0;
       }
       // beyond the staged values (tiles with more escapes than kDecValCap):
       // the compact loop over set bits, values from global memory (the
