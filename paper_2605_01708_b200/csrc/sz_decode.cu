@@ -562,9 +562,11 @@ struct DecSmem {
   uint64_t empty[STAGES];
 };
 
-template <int FMT, int CB, int POSB>
+template <int FMT, int CB, int PMODE>
 __global__ void __launch_bounds__(kDecThreads, 2)
     decode_persistent(const __grid_constant__ sz_params p, const DecodeArgs a) {
+  // PMODE = position bytes (1, 2, 4 abs32), 0 sentinel, kPosMarked (K3e)
+  constexpr int POSB = PMODE;
   constexpr int EPV = kEpv<FMT>;
   constexpr int G = EPV / 4;
   constexpr int WB = Fmt<FMT>::kWordBytes;
@@ -1259,9 +1261,10 @@ struct DecodeWs {
 // Escape-dense chunk-relative streams take the K3e path (bitmap pre-pass)
 // when the declared M reaches 1/kDenseDiv of N.  The crossover was measured
 // with SZ_DEC_MARKED=0/1 (forces either path; tuning and tests only) at 2^31
-// words (profiles/bench_dense_r02.jsonl): the stager walk wins up to ~2.4%
-// escapes, K3e from ~4% (BF16 7.89%: 1227 -> 1720 GB/s).
-constexpr uint64_t kDenseDiv = 32;
+// words (profiles/bench_dense_r02.jsonl): with the branch-free group merge
+// the stager walk wins below ~1.8% escapes, K3e above ~2% (BF16 7.89%:
+// 1227 -> 1921 GB/s).
+constexpr uint64_t kDenseDiv = 50;
 int marked_override() {
   const char* e = getenv("SZ_DEC_MARKED");   // read per call: tests force both paths
   return e && *e ? atoi(e) : -1;

@@ -24,6 +24,7 @@ N = int(os.environ.get("SZ_DENSE_N", 1 << 31))
 RATES = [float(r) for r in os.environ.get(
     "SZ_DENSE_RATES", "0.0016,0.004,0.008,0.012,0.016,0.024,0.04,0.0789").split(",")]
 FMTS = os.environ.get("SZ_DENSE_FMTS", "bf16,e5m2").split(",")
+PATHS = os.environ.get("SZ_DENSE_PATHS", "0,1").split(",")
 
 
 def profile(fmt):
@@ -66,7 +67,7 @@ def main():
             # for K3e when M calls for it)
             eng.dec_ws = torch.empty(eng.lib.sz_decode_workspace_bytes(N, N, eng.params),
                                      dtype=torch.uint8, device=eng.device)
-            for path in ("0", "1"):
+            for path in PATHS:
                 os.environ["SZ_DEC_MARKED"] = path
                 ms = timed_decode(eng, words)
                 print(json.dumps({"config": name, "path": {"0": "stager", "1": "k3e"}[path],
