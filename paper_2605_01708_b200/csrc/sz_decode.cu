@@ -297,61 +297,66 @@ __global__ void __launch_bounds__(kMarkWarps * 32) escape_marks_kernel(const Mar
           vv[u] = in ? static_cast<uint32_t>(vb[32 * u]) : 0u;
         }
       };
+      // one round of 32 ordinals; the bitmap OR is unconditional (a lane
+      // without a hit ORs 0 into word 0), the chunk search branch is
+      // warp-uniform (__any_sync), so the only divergent branch left is the
+      // rare failed check
+      auto round = [&](uint32_t br, uint32_t pv, uint32_t v) {
+        const uint32_t orl = br + lane, last = min(br + 31, no - 1);
+        uint32_t k = cur;
+        if (__any_sync(0xffffffffu, cur + 2 <= nk && srel[cur + 2] <= last)) {
+          uint32_t hi = nk;
+          while (hi - k > 1) {
+            const uint32_t mid = (k + hi) >> 1;
+            if (srel[mid] <= orl) k = mid; else hi = mid;
+          }
+        } else {
+          k += cur + 1 < nk && srel[cur + 1] <= orl ? 1u : 0u;
+        }
+        // an ordinal is its chunk's first exactly when its predecessor is
+        // in another chunk (offsets are monotone)
+        uint32_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
+        uint32_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
+        if (lane == 0) {
+          kprev = carry_k;
+          prev = carry_pv;
+        }
+        cur = __shfl_sync(0xffffffffu, k, 31);
+        carry_k = cur;
+        carry_pv = __shfl_sync(0xffffffffu, pv, 31);
+        const int32_t rel = kbase + static_cast<int32_t>(k * chunk32 + pv);
+        const bool live = orl < no;
+        // one set test covers the domain and the in-book check
+        const bool val_ok = (s_esc_ok[v >> 5] >> (v & 31)) & 1u;
+        const bool over = pv >= chunk32, beyond = rel >= past;
+        const bool not_inc = k == kprev && prev >= pv;
+        if (__builtin_expect(live && (!val_ok || over || beyond || not_inc), 0)) {
+          // rare: the reference's checks in order (codec.py:446-536)
+          const uint64_t o = o_lo + orl;
+          if (v >= a.exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+          else if (!val_ok) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+          if (over) record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
+          else if (beyond) record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
+          else if (not_inc) record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
+        }
+        const bool hit = live && !over && static_cast<uint32_t>(rel) < span;
+        const uint32_t ur = hit ? static_cast<uint32_t>(rel) : 0u;
+        atomicOr(&S.bits[ur >> 5], hit ? 1u << (ur & 31) : 0u);
+      };
+      // ping-pong batches: the next batch's loads land in the other register
+      // set while this one is processed (no register copies)
+      uint32_t qpvs[U], qvs[U];
       if (no) load_batch(0, pvs, vs);
-      for (uint32_t b0 = 0; b0 < no; b0 += 32 * U) {
-        uint32_t npvs[U], nvs[U];
-        if (b0 + 32 * U < no) load_batch(b0 + 32 * U, npvs, nvs);
+      for (uint32_t b0 = 0; b0 < no; b0 += 64 * U) {
+        if (b0 + 32 * U < no) load_batch(b0 + 32 * U, qpvs, qvs);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t br = b0 + 32 * u;
-          if (br >= no) break;
-          const uint32_t orl = br + lane, last = min(br + 31, no - 1);
-          const uint32_t pv = pvs[u], v = vs[u];
-          uint32_t k = cur;
-          const bool multi = cur + 2 <= nk && srel[cur + 2] <= last;  // (warp-uniform)
-          if (__builtin_expect(multi, 0)) {
-            uint32_t hi = nk;
-            while (hi - k > 1) {
-              const uint32_t mid = (k + hi) >> 1;
-              if (srel[mid] <= orl) k = mid; else hi = mid;
-            }
-          } else {
-            k += cur + 1 < nk && srel[cur + 1] <= orl ? 1u : 0u;
-          }
-          // an ordinal is its chunk's first exactly when its predecessor is
-          // in another chunk (offsets are monotone)
-          uint32_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
-          uint32_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
-          if (lane == 0) {
-            kprev = carry_k;
-            prev = carry_pv;
-          }
-          cur = __shfl_sync(0xffffffffu, k, 31);
-          carry_k = cur;
-          carry_pv = __shfl_sync(0xffffffffu, pv, 31);
-          const int32_t rel = kbase + static_cast<int32_t>(k * chunk32 + pv);
-          const bool live = orl < no;
-          // one set test covers the domain and the in-book check
-          const bool val_ok = (s_esc_ok[v >> 5] >> (v & 31)) & 1u;
-          const bool over = pv >= chunk32, beyond = rel >= past;
-          const bool not_inc = k == kprev && prev >= pv;
-          if (__builtin_expect(live && (!val_ok || over || beyond || not_inc), 0)) {
-            // rare: the reference's checks in order (codec.py:446-536)
-            const uint64_t o = o_lo + orl;
-            if (v >= a.exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-            else if (!val_ok) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-            if (over) record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
-            else if (beyond) record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
-            else if (not_inc) record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
-          }
-          if (live && !over && static_cast<uint32_t>(rel) < span)
-            atomicOr(&S.bits[static_cast<uint32_t>(rel) >> 5], 1u << (rel & 31));
-        }
+        for (int u = 0; u < U; ++u)
+          if (b0 + 32 * u < no) round(b0 + 32 * u, pvs[u], vs[u]);
+        if (b0 + 32 * U >= no) break;
+        if (b0 + 64 * U < no) load_batch(b0 + 64 * U, pvs, vs);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          pvs[u] = npvs[u];
-          vs[u] = nvs[u];
-        }
+        for (int u = 0; u < U; ++u)
+          if (b0 + 32 * (U + u) < no) round(b0 + 32 * (U + u), qpvs[u], qvs[u]);
       }
     } else {
       // corrupt counts (> 2^31 ordinals in one window): plain per-ordinal
@@ -541,9 +546,9 @@ constexpr int kDecHelpers = 3;                          // escape-staging warps
 constexpr int kPosMarked = 8;   // K4 POSB of escape-dense chunk-relative streams (K3e)
 constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
 constexpr int kDecOffStage = 64;                        // staged chunk offsets per helper
-template <int FMT>
+template <int FMT, int NSTAGES = 5>
 struct DecSmem {
-  static constexpr int STAGES = 5;
+  static constexpr int STAGES = NSTAGES;
   static constexpr int EPV = kEpv<FMT>;
   static constexpr int TILE = kDecSlots * EPV;
   alignas(128) uint8_t codes[STAGES][TILE / 2];              // <= 4-bit codes
@@ -562,8 +567,16 @@ struct DecSmem {
   uint64_t empty[STAGES];
 };
 
+// The K3e instantiation runs 3 CTAs per SM (24 decode warps instead of 16:
+// its escape merge is latency-bound) on a shallower ring: 4 stages (BF16) /
+// 3 (FP8) keep 3 CTAs' shared memory within the SM, 56 registers the file.
+template <int FMT, int PMODE>
+constexpr int kDecStages = PMODE == kPosMarked ? (FMT == SZ_BF16 ? 4 : 3) : 5;
+template <int PMODE>
+constexpr int kDecCtasPerSm = PMODE == kPosMarked ? 3 : 2;
+
 template <int FMT, int CB, int PMODE>
-__global__ void __launch_bounds__(kDecThreads, 2)
+__global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<PMODE>)
     decode_persistent(const __grid_constant__ sz_params p, const DecodeArgs a) {
   // PMODE = position bytes (1, 2, 4 abs32), 0 sentinel, kPosMarked (K3e)
   constexpr int POSB = PMODE;
@@ -588,7 +601,7 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   constexpr bool kGroupMerge = POSB == kPosMarked;
   constexpr int LUT2 = CB == 4 ? 256 : 64;
   constexpr uint32_t kCodeMask = (1u << CB) - 1;
-  using Smem = DecSmem<FMT>;
+  using Smem = DecSmem<FMT, kDecStages<FMT, PMODE>>;
   constexpr int kStages = Smem::STAGES;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -1362,7 +1375,7 @@ cudaError_t launch_marks(const MarkArgs& ma, cudaStream_t s) {
 template <int FMT, int CB, int POSB>
 cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
   auto kern = decode_persistent<FMT, CB, POSB>;
-  const int smem = static_cast<int>(sizeof(DecSmem<FMT>));
+  const int smem = static_cast<int>(sizeof(DecSmem<FMT, kDecStages<FMT, POSB>>));
   const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kDecThreads);
   if (ks.err != cudaSuccess) return ks.err;
   const int per_sm = ks.per_sm < 1 ? 1 : ks.per_sm;
