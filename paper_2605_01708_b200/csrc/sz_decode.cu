@@ -567,16 +567,21 @@ struct DecSmem {
   uint64_t empty[STAGES];
 };
 
-// The K3e instantiation runs 3 CTAs per SM (24 decode warps instead of 16:
-// its escape merge is latency-bound) on a shallower ring: 4 stages (BF16) /
-// 3 (FP8) keep 3 CTAs' shared memory within the SM, 56 registers the file.
+// CTAs per SM and ring depth.  The K3e instantiation and every E5M2 decoder
+// run 3 CTAs per SM (24 decode warps instead of 16) on a shallower ring — 4
+// stages (BF16) / 3 (FP8) keep 3 CTAs' shared memory within the SM, 56
+// registers the file: the K3e merge is latency-bound (BF16 top-8 3-bit
+// 2016 -> 2059 GB/s) and so is E5M2's decode (c3 2925 -> 2999 GB/s,
+// alternating A/B runs on one box).  Realistic BF16 keeps 2 x 5 stages (it
+// runs at the copy peak).
 template <int FMT, int PMODE>
-constexpr int kDecStages = PMODE == kPosMarked ? (FMT == SZ_BF16 ? 4 : 3) : 5;
-template <int PMODE>
-constexpr int kDecCtasPerSm = PMODE == kPosMarked ? 3 : 2;
+constexpr int kDecStages = PMODE == kPosMarked ? (FMT == SZ_BF16 ? 4 : 3)
+                                               : (FMT == SZ_E5M2 ? 3 : 5);
+template <int FMT, int PMODE>
+constexpr int kDecCtasPerSm = PMODE == kPosMarked || FMT == SZ_E5M2 ? 3 : 2;
 
 template <int FMT, int CB, int PMODE>
-__global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<PMODE>)
+__global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
     decode_persistent(const __grid_constant__ sz_params p, const DecodeArgs a) {
   // PMODE = position bytes (1, 2, 4 abs32), 0 sentinel, kPosMarked (K3e)
   constexpr int POSB = PMODE;
