@@ -49,6 +49,8 @@ CASES = [  # fmt, chunk, rate, code bits, n
     (0, 1000, 0.07, 4, 3 * 8192 + 5),          # chunk not dividing the tile
     (0, 48, 0.1, 3, 3 * 8192 + 100),           # chunk not a power of two, < a bitmap window word run
     (0, 16384, 0.07, 4, 5 * 8192),             # chunk larger than the decode tile
+    (0, 65536, 0.07, 4, 3 * 65536 + 100),      # chunk spanning 4 K3e windows
+    (1, 32, 0.1, 3, 2 * 16384 + 999),          # the smallest chunk K3e takes
     (1, 1024, 0.0789, 4, 3 * 16384 + 77), (1, 1024, 0.0689, 3, 4 * 16384),
     (1, 16384, 0.3, 4, 2 * 16384 + 1), (1, 128, 0.05, 3, 3 * 16384 + 3),
     (2, 1024, 0.07, 3, 3 * 16384 + 11), (2, 512, 1.0, 3, 16384 + 5),
