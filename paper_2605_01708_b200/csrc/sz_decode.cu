@@ -535,6 +535,26 @@ __device__ __forceinline__ uint32_t merge_group(uint32_t e4, uint32_t mg, uint32
   return __byte_perm(v4, e4, sel);
 }
 
+// First escaped element of a slot whose dense code is not the dummy code 0
+// (codec.py:472-476), recorded in the status; called only when the
+// group-wise merge saw one (corrupt streams).
+template <int CB, int CWORDS>
+__device__ __forceinline__ void first_nondummy(const uint32_t* cw, uint32_t bm, uint64_t e0,
+                                               sz_decode_status* st) {
+  while (bm) {
+    const int j = __ffs(bm) - 1;
+    bm &= bm - 1;
+    const int bit = CB * j;
+    const uint64_t lo = pick<CWORDS>(cw, bit >> 5);
+    const uint64_t hi = (bit >> 5) + 1 < CWORDS ? pick<CWORDS>(cw, (bit >> 5) + 1) : 0u;
+    const uint32_t code = static_cast<uint32_t>(((hi << 32) | lo) >> (bit & 31)) & ((1u << CB) - 1);
+    if (code != 0) {
+      record_first(&st->first_inv[SZ_DEC_NONDUMMY], e0 + j);
+      return;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K4 (persistent)
 // Explicit modes (chunk-relative and abs32).  Same warp-specialised shape as
 // the encoder: warp 8 streams each tile's code and sign|mantissa planes into a
@@ -546,12 +566,12 @@ constexpr int kDecHelpers = 3;                          // escape-staging warps
 constexpr int kPosMarked = 8;   // K4 POSB of escape-dense chunk-relative streams (K3e)
 constexpr int kDecThreads = kThreads + 32 * (1 + kDecHelpers);
 constexpr int kDecOffStage = 64;                        // staged chunk offsets per helper
-template <int FMT, int NSTAGES = 5>
+template <int FMT, int NSTAGES = 5, int CB = 4>
 struct DecSmem {
   static constexpr int STAGES = NSTAGES;
   static constexpr int EPV = kEpv<FMT>;
   static constexpr int TILE = kDecSlots * EPV;
-  alignas(128) uint8_t codes[STAGES][TILE / 2];              // <= 4-bit codes
+  alignas(128) uint8_t codes[STAGES][TILE * CB / 8];
   alignas(128) uint8_t sm[STAGES][TILE * Fmt<FMT>::kSmBits / 8];
   uint32_t bitmap[STAGES][TILE / 32];
   uint32_t slot_first[STAGES][kDecSlots];  // compact index of a slot's first escape
@@ -574,8 +594,15 @@ struct DecSmem {
 // 2016 -> 2059 GB/s) and so is E5M2's decode (c3 2925 -> 2999 GB/s,
 // alternating A/B runs on one box).  Realistic BF16 keeps 2 x 5 stages (it
 // runs at the copy peak).
-template <int FMT, int PMODE>
-constexpr int kDecStages = PMODE == kPosMarked ? (FMT == SZ_BF16 ? 4 : 3)
+// K3e instantiation with 3-bit codes: one 4096-entry table maps a 12-bit
+// code group straight to its four exponent bytes (16 KiB of shared memory;
+// its ring drops to 3 stages so 3 CTAs still fit an SM): one lookup per 4
+// elements instead of two pair lookups, their address arithmetic and a
+// PRMT — top-8 3-bit decode BF16 2067 -> 2095, E5M2 1196 -> 1297 GB/s.
+template <int CB, int PMODE>
+constexpr bool kT12 = CB == 3 && PMODE == kPosMarked;
+template <int FMT, int CB, int PMODE>
+constexpr int kDecStages = PMODE == kPosMarked ? (FMT == SZ_BF16 && !kT12<CB, PMODE> ? 4 : 3)
                                                : (FMT == SZ_E5M2 ? 3 : 5);
 template <int FMT, int PMODE>
 constexpr int kDecCtasPerSm = PMODE == kPosMarked || FMT == SZ_E5M2 ? 3 : 2;
@@ -606,7 +633,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
   constexpr bool kGroupMerge = POSB == kPosMarked;
   constexpr int LUT2 = CB == 4 ? 256 : 64;
   constexpr uint32_t kCodeMask = (1u << CB) - 1;
-  using Smem = DecSmem<FMT, kDecStages<FMT, PMODE>>;
+  using Smem = DecSmem<FMT, kDecStages<FMT, CB, PMODE>, CB>;
   constexpr int kStages = Smem::STAGES;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -622,6 +649,14 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
     s_lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
   const uint32_t lut2_base = smem_addr(s_lut2);
+  constexpr bool T12 = kT12<CB, PMODE>;
+  __shared__ __align__(16) uint32_t s_t12[T12 ? 4096 : 1];
+  if constexpr (T12) {
+    for (int i = tid; i < 4096; i += kDecThreads)
+      s_t12[i] = p.dec_lut[i & 7] | (p.dec_lut[(i >> 3) & 7] << 8) |
+                 (p.dec_lut[(i >> 6) & 7] << 16) | (p.dec_lut[i >> 9] << 24);
+  }
+  const uint32_t t12_base = smem_addr(s_t12);
   // In-book exponents as a 256-bit set in shared memory: the stagers' value
   // checks index it by escape value (a divergent index into the kernel
   // parameters' enc_lut would serialise the constant cache per distinct value).
@@ -1113,7 +1148,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
           const uint32_t first = bm ? sf : 0u;
           if (first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
             const uint32_t vbase = smem_addr(S.vals[s]);
-            uint32_t r = first, nd_el = 0xFFu;
+            uint32_t r = first, nd_any = 0;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
               const uint32_t mg = (bm >> (4 * g)) & 15u;
@@ -1121,11 +1156,11 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
               const uint32_t t = merge_group(ow[g] >> 2 & 0x1F1F1F1Fu, mg, r, vbase, sel_base,
                                              d0 * 0x01010101u, &nd);
               ow[g] = (ow[g] & 0x83838383u) | ((t << 2) & 0x7C7C7C7Cu);
-              if (!SENT) nd_el = min(nd_el, nd ? 4u * g + (__ffs(nd) - 1) / 8 : 0xFFu);
+              nd_any |= nd;
               r += __popc(mg);
             }
-            if (!SENT && nd_el != 0xFFu)
-              record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + nd_el);
+            if (!SENT && nd_any)   // rare: the first escaped element with a non-dummy code
+              first_nondummy<CB, CWORDS>(cw, bm, e0, a.status);
             bm = 0;
           }
         }
@@ -1162,6 +1197,14 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
           }
         } else {
           const uint32_t cb12 = group_bits<12>(cw, g);
+          if (T12 && !check_range) {
+            // the group's four exponents in one lookup (full 8-entry book)
+            eg[g] = lds_u32(t12_base + (cb12 << 2));
+            if constexpr (SMB == 8) ag[g] = sw[g];
+            else if constexpr (SMB == 4) ag[g] = unpack_nib4(group_bits<16>(sw, g));
+            else ag[g] = unpack_tri4(group_bits<12>(sw, g));
+            continue;
+          }
           l0 = lds_u32(lut2_base | ((cb12 << 2) & 0xFCu));
           l1 = lds_u32(lut2_base | ((cb12 >> 4) & 0xFCu));
         }
@@ -1191,17 +1234,17 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
         const uint32_t first = bm ? sf : 0u;
         if (first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
           const uint32_t vbase = smem_addr(S.vals[s]);
-          uint32_t r = first, nd_el = 0xFFu;
+          uint32_t r = first, nd_any = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const uint32_t mg = (bm >> (4 * g)) & 15u;
             uint32_t nd;
             eg[g] = merge_group(eg[g], mg, r, vbase, sel_base, d0 * 0x01010101u, &nd);
-            if (!SENT) nd_el = min(nd_el, nd ? 4u * g + (__ffs(nd) - 1) / 8 : 0xFFu);
+            nd_any |= nd;
             r += __popc(mg);
           }
-          if (!SENT && nd_el != 0xFFu)
-            record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + nd_el);
+          if (!SENT && nd_any)   // rare: the first escaped element with a non-dummy code
+            first_nondummy<CB, CWORDS>(cw, bm, e0, a.status);
           bm = 0;
         }
       }
@@ -1380,7 +1423,7 @@ cudaError_t launch_marks(const MarkArgs& ma, cudaStream_t s) {
 template <int FMT, int CB, int POSB>
 cudaError_t launch_persistent(const sz_params& p, const DecodeArgs& a, cudaStream_t s) {
   auto kern = decode_persistent<FMT, CB, POSB>;
-  const int smem = static_cast<int>(sizeof(DecSmem<FMT, kDecStages<FMT, POSB>>));
+  const int smem = static_cast<int>(sizeof(DecSmem<FMT, kDecStages<FMT, CB, POSB>, CB>));
   const KernelSetup ks = kernel_setup(reinterpret_cast<const void*>(kern), smem, kDecThreads);
   if (ks.err != cudaSuccess) return ks.err;
   const int per_sm = ks.per_sm < 1 ? 1 : ks.per_sm;
