@@ -794,11 +794,54 @@ struct GatherArgs {
   uint32_t split;                 // CTAs per group (record moves split R ways)
 };
 
+// Warp copy of nbytes from a 4-byte-aligned source to an arbitrary
+// destination: destination word w holds source bytes [4w - sh, 4w - sh + 4),
+// sh = the destination's misalignment, built from source words w-1 (from the
+// neighbouring lane) and w by one funnel shift; the partial first / last
+// words are written bytewise (their other bytes belong to neighbouring runs).
+__device__ __forceinline__ void warp_copy_bytes(uint8_t* dst, const uint8_t* src,
+                                                uint32_t nbytes, int lane) {
+  if (nbytes == 0) return;
+  const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 3u);
+  uint8_t* const d0 = dst - sh;
+  const uint32_t* const sw = reinterpret_cast<const uint32_t*>(src);
+  const uint32_t nwords = (sh + nbytes + 3) >> 2;
+  constexpr int U = 4;   // rounds per step: all their loads in flight first
+  uint32_t carry = 0;    // source word (base - 1), from the previous round's lane 31
+  for (uint32_t base = 0; base < nwords; base += 32 * U) {
+    uint32_t hi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t w = base + 32 * u + lane;
+      hi[u] = 4 * w < nbytes ? __ldg(sw + w) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t w = base + 32 * u + lane;
+      uint32_t lo = __shfl_up_sync(0xffffffffu, hi[u], 1);
+      if (lane == 0) lo = carry;
+      carry = __shfl_sync(0xffffffffu, hi[u], 31);
+      if (w < nwords) {
+        const uint32_t v = sh ? __funnelshift_l(lo, hi[u], 8 * sh) : hi[u];
+        // bytes of this word inside [sh, sh + nbytes) of the destination span
+        const uint32_t b0 = 4 * w, b1 = b0 + 4;
+        if (b0 >= sh && b1 <= sh + nbytes) {
+          *reinterpret_cast<uint32_t*>(d0 + b0) = v;
+        } else {
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i)
+            if (b0 + i >= sh && b0 + i < sh + nbytes) d0[b0 + i] = static_cast<uint8_t>(v >> (8 * i));
+        }
+      }
+    }
+  }
+}
+
 // Tiles per CTA: 256 (8 per lane in the scan) keeps the look-back chain
 // short — K2b is latency-bound, so fewer, fatter CTAs win.
 constexpr int kGatherTiles = 256;
-static_assert(kGatherTiles == 256, "escape_gather's search does exactly 8 halvings");
 constexpr int kGatherUnroll = 4;
+static_assert(kGatherTiles == 256, "escape_gather's search does exactly 8 halvings");
 
 template <int FMT, int POSB>
 __global__ void __launch_bounds__(kThreads)
@@ -922,6 +965,29 @@ __global__ void __launch_bounds__(kThreads)
       for (int u = 0; u < TU; ++u)  // tiles with more than 32 records (rare here)
         for (uint32_t r = lane + 32; r < cnt[u]; r += 32)
           if (dst[u] - lane + r < a.capacity) move(src[u] - lane + r, dst[u] - lane + r);
+    }
+  } else if (rpref[kGatherTiles] > 512u * kGatherTiles) {
+    // Escape-dense groups (> 512 records per tile on average): a tile's records are one contiguous run in its
+    // scratch slot and one contiguous run in each output section, so a warp
+    // moves a whole (tile, section) run as 32-bit words realigned with a
+    // funnel shift (the scratch slot is 16-byte aligned, the destination
+    // arbitrary): coalesced 128-byte warp accesses instead of a byte or u16
+    // per record, and no per-record tile search.
+    const int k_lo = static_cast<int>(kGatherTiles * part / a.split);
+    const int k_hi = static_cast<int>(kGatherTiles * (part + 1) / a.split);
+    const int items = 2 * (k_hi - k_lo);   // (tile, values | positions)
+    for (int it = warp; it < items; it += kWarps) {
+      const int k = k_lo + (it >> 1);
+      const uint32_t cnt = tcnt[k];
+      if (cnt == 0 || cnt > kTileCap<FMT>) continue;   // empty, or heavy (K2c's)
+      const uint64_t dst = tpref[k];
+      if (dst >= a.capacity) continue;
+      const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(cnt), a.capacity - dst));
+      const uint64_t src = (t0 + k) * kTileCap<FMT>;
+      if ((it & 1) == 0)
+        warp_copy_bytes(a.values + dst, a.scr_val + src, n, lane);
+      else if constexpr (POSB != 0)
+        warp_copy_bytes(a.positions + dst * POSB, a.scr_pos + src * POSB, n * POSB, lane);
     }
   } else {
     const uint64_t g_all = rpref[kGatherTiles];
@@ -1186,23 +1252,48 @@ __global__ void __launch_bounds__(kThreads)
 // K6: raw exponent bytes -> dense LE bitstream of `width` bits per value
 // (_pack_values / _pack_bits, codec.py:241-266).  Reads M from device memory
 // so it chains after the encoder without a host round trip.
-__global__ void pack_values_kernel(const uint8_t* __restrict__ vals, const uint64_t* m_ptr,
-                                   uint64_t capacity, int width, uint8_t* __restrict__ out) {
+// FP8 escape values -> 5 / 4-bit little-endian stream (formats.py:167-189).
+// A thread packs 8 values (one 8-byte load) into `width` bytes; a block's
+// 256 x width output bytes are contiguous and 4-byte aligned, so they go
+// through shared memory and leave as coalesced 32-bit stores.
+__global__ void __launch_bounds__(kThreads)
+    pack_values_kernel(const uint8_t* __restrict__ vals, const uint64_t* m_ptr,
+                       uint64_t capacity, int width, uint8_t* __restrict__ out) {
+  __shared__ __align__(16) uint8_t sbuf[kThreads * 8];
   const uint64_t m = min(*m_ptr, capacity);
   const uint64_t groups = (m + 7) / 8;
-  for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; gi < groups;
-       gi += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  const uint64_t nbytes_total = (m * width + 7) / 8;
+  const int tid = threadIdx.x;
+  const bool v8 = !(reinterpret_cast<uintptr_t>(vals) & 7);
+  const bool o4 = !(reinterpret_cast<uintptr_t>(out) & 3);
+  for (uint64_t blk = blockIdx.x; blk * kThreads < groups; blk += gridDim.x) {
+    const uint64_t gi = blk * kThreads + tid;
     uint64_t acc = 0;
-    for (int j = 0; j < 8; ++j) {
-      const uint64_t o = gi * 8 + j;
-      const uint64_t v = o < m ? vals[o] : 0;
-      acc |= v << (j * width);
+    if (gi < groups) {
+      uint64_t x;
+      if (v8 && gi * 8 + 8 <= m) {
+        x = __ldg(reinterpret_cast<const unsigned long long*>(vals) + gi);
+      } else {
+        x = 0;
+        for (int j = 0; j < 8; ++j)
+          if (gi * 8 + j < m) x |= static_cast<uint64_t>(vals[gi * 8 + j]) << (8 * j);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc |= ((x >> (8 * j)) & 0xFFu) << (j * width);
     }
-    const uint64_t nbytes_total = (m * width + 7) / 8;
-    for (int b = 0; b < width; ++b) {
-      const uint64_t ob = gi * width + b;
-      if (ob < nbytes_total) out[ob] = static_cast<uint8_t>(acc >> (8 * b));
+    for (int b = 0; b < width; ++b) sbuf[tid * width + b] = static_cast<uint8_t>(acc >> (8 * b));
+    __syncthreads();
+    const uint64_t ob0 = blk * kThreads * width;   // multiple of 4 (kThreads x width)
+    for (int w = tid; w < kThreads * width / 4; w += kThreads) {
+      const uint64_t ob = ob0 + 4ull * w;
+      if (o4 && ob + 4 <= nbytes_total) {
+        *reinterpret_cast<uint32_t*>(out + ob) = reinterpret_cast<const uint32_t*>(sbuf)[w];
+      } else {
+        for (int b = 0; b < 4; ++b)
+          if (ob + b < nbytes_total) out[ob + b] = sbuf[4 * w + b];
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -1513,9 +1604,13 @@ int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shi
   // (append mode: the caller packs the whole stream once, after the last piece)
   if (exp_bits != 8 && out->escape_capacity && !out->d_escape_base) {
     if (!out->d_values_packed) return SZ_ECONFIG;
-    pack_values_kernel<<<296, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
-                                                out->escape_capacity, exp_bits,
-                                                out->d_values_packed);
+    // one block per 2048 values of the capacity (blocks past M exit at once),
+    // at most 16 per SM with a grid-stride loop beyond
+    const uint64_t want = (out->escape_capacity + 8 * kThreads - 1) / (8 * kThreads);
+    const unsigned pg = static_cast<unsigned>(want < 148 * 16 ? (want ? want : 1) : 148 * 16);
+    pack_values_kernel<<<pg, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
+                                               out->escape_capacity, exp_bits,
+                                               out->d_values_packed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
