@@ -181,6 +181,11 @@ int sz_encode(const void* d_words, uint64_t n, const sz_params* p,
               const sz_encoded* out, void* d_ws, size_t ws_bytes, void* stream);
 
 /* ---- K4 decode (codec.py:421-536) --------------------------------------- */
+/* m: the escape count the decode will declare (n = size for any M).  For
+ * chunk-relative streams with chunk >= 32 and M >= N/50 the workspace also
+ * holds the escape-dense path's element bitmap (N/8 bytes) and per-tile
+ * counts; sz_decode takes that path only when the workspace it is given is
+ * large enough (else the general path, correct for any M). */
 size_t sz_decode_workspace_bytes(uint64_t n, uint64_t m, const sz_params* p);
 int sz_decode(const sz_encoded_in* in, const sz_params* p, void* d_words_out,
               sz_decode_status* d_status, void* d_ws, size_t ws_bytes, void* stream);
