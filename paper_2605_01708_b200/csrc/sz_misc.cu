@@ -49,7 +49,10 @@ __global__ void __launch_bounds__(kThreads) hist_kernel(const uint8_t* __restric
   using C = HistCfg<FMT>;
   constexpr int EPV = kEpv<FMT>;
   constexpr int WB = Fmt<FMT>::kWordBytes;
-  constexpr int UNROLL = 4;
+#ifndef SZ_K1_UNROLL
+#define SZ_K1_UNROLL 8
+#endif
+  constexpr int UNROLL = SZ_K1_UNROLL;
   extern __shared__ uint32_t hsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < C::kSmemWords; i += kThreads) hsm[i] = 0;
