@@ -203,10 +203,11 @@ class GpuPieceCodec:
     def _workspace(self, kind: str, n: int, m: int) -> torch.Tensor:
         need = (self.lib.sz_encode_workspace_bytes(n, self.params) if kind == "enc"
                 else self.lib.sz_decode_workspace_bytes(n, m, self.params))
-        ws = self._ws.get((kind, n))
+        key = (kind, n, kind == "dec" and m > 0)   # (regular and spill decodes apart)
+        ws = self._ws.get(key)
         if ws is None or ws.numel() < need:
             ws = torch.empty(need, dtype=torch.uint8, device=self.device)
-            self._ws[(kind, n)] = ws
+            self._ws[key] = ws
         return ws
 
     def _encoded(self, lay: FrameLayout, fr: torch.Tensor):
@@ -274,7 +275,11 @@ class GpuPieceCodec:
         src.n_escapes = lay.capacity          # capacity; M comes from the header
         src.n_counts = cfg.n_chunks(n) if cfg.chunked else 0
         src.d_n_escapes = frame.data_ptr() + 8
-        ws = self._workspace("dec", n, lay.capacity)
+        # M is read on the device, so the escape-dense decoder path (K3e) is
+        # chosen from the workspace: sized for it only for spill frames (their
+        # capacity is the piece's exact, dense M); a regular frame's capacity
+        # (N/32) says nothing about its M
+        ws = self._workspace("dec", n, lay.capacity if capacity is not None else 0)
         status = torch.empty(N.STATUS_BYTES, dtype=torch.uint8, device=self.device)
         N.check(self.lib.sz_decode(src, self.params, N.ptr(out), N.ptr(status), N.ptr(ws),
                                    ws.numel(), N.stream_handle()), "decode")
