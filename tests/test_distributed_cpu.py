@@ -182,3 +182,35 @@ def test_sharded_sections_concatenate_to_global():
         assert b"".join(x[key] for x in parts) == whole[key]
     for key in ("chunk_counts", "escape_positions", "escape_values"):
         assert np.array_equal(np.concatenate([x[key] for x in parts]), whole[key])
+
+
+@pytest.mark.parametrize("fmt_name,cb,chunk,n,cap", [
+    ("bf16", 4, 1024, 1 << 20, 1 << 15), ("bf16", 3, 256, 70_001, 4096),
+    ("e5m2", 4, 1024, 1 << 20, 1 << 15), ("e4m3", 3, 64, 12_345, 12_345),
+])
+def test_frame_layout_offsets(fmt_name, cb, chunk, n, cap):
+    """FrameLayout: a 16-byte header, then counts, codes, sign|mantissa,
+    positions, values in serialization order (codec.py:176-184), each
+    256-byte aligned (the decoder reads codes / sign|mantissa with 16-byte
+    bulk copies), the wire ending after the values, FP8's packed-values
+    scratch after the wire."""
+    import paper_2605_01708_b200 as sz
+    from paper_2605_01708_b200.distributed import FrameLayout
+    from paper_2605_01708_b200.formats import packed_nbytes
+    fmt = sz.ElementFormat.from_name(fmt_name)
+    cfg = sz.CodecConfig(fmt, cb, chunk_size=chunk)
+    lay = FrameLayout(cfg, n, cap)
+    order = ["counts", "codes", "sm", "positions", "values"]
+    assert [lay.off[k] for k in order] == sorted(lay.off[k] for k in order)
+    assert lay.off["counts"] >= 16
+    for k in order:
+        assert lay.off[k] % 256 == 0
+    assert lay.size["counts"] == 4 * cfg.n_chunks(n)
+    assert lay.size["codes"] == packed_nbytes(n, cb)
+    assert lay.size["sm"] == cfg.sm_nbytes(n)
+    assert lay.size["positions"] == cap * cfg.position_nbytes
+    assert lay.size["values"] == cap
+    assert lay.wire_bytes >= lay.off["values"] + cap
+    assert lay.packed_off >= lay.wire_bytes
+    extra = packed_nbytes(cap, fmt.exp_bits) if fmt.exp_bits != 8 else 0
+    assert lay.total >= lay.packed_off + extra
