@@ -308,8 +308,9 @@ def run_ours(args) -> None:
         ev[k][2].record(stream)
     torch.cuda.synchronize()
     barrier()
-    enc_ms = sum(ev[k][0].elapsed_time(ev[k][1]) for k in range(K))
-    dec_ms = sum(ev[k][1].elapsed_time(ev[k][2]) for k in range(K))
+    enc_each = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    dec_each = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    enc_ms, dec_ms = sum(enc_each), sum(dec_each)
     tot_ms = ev[0][0].elapsed_time(ev[K - 1][2])
     per_rank_ms = [tot_ms]
     if world > 1:
@@ -400,6 +401,12 @@ def run_ours(args) -> None:
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round(tot_ms / K, 4),
+        # SURVEY §8(d) timing protocol: mean +- stdev of the per-step device
+        # times (this rank)
+        "step_ms_stats": {"encode_mean": round(statistics.mean(enc_each), 4),
+                          "encode_stdev": round(statistics.pstdev(enc_each), 4),
+                          "decode_mean": round(statistics.mean(dec_each), 4),
+                          "decode_stdev": round(statistics.pstdev(dec_each), 4)},
         "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
         "dtype": "u16" if fmt.word_bits == 16 else "u8", "data": "synthetic",
         "config": bench_config(wl, args, n, book.entries),
