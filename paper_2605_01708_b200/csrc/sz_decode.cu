@@ -234,15 +234,16 @@ struct alignas(16) MarkSmem {
   uint32_t srel[kMarkMaxChunks];   // chunk starts as ordinals relative to the window's first
 };
 static_assert(sizeof(MarkSmem) % 16 == 0, "per-warp K3e state stays 16-byte aligned");
+static_assert(kMarkWarps * 32 == 256, "one thread per entry of the K3e value table");
 
 template <int POSB>
 __global__ void __launch_bounds__(kMarkWarps * 32) escape_marks_kernel(const MarkArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int lane = threadIdx.x & 31;
   MarkSmem& S = reinterpret_cast<MarkSmem*>(smem_raw)[threadIdx.x >> 5];
-  __shared__ uint32_t s_esc_ok[8];
+  __shared__ uint8_t s_vbad[256];     // 1: not a valid escape value (domain or in the book)
   pdl_trigger();
-  if (threadIdx.x < 8) s_esc_ok[threadIdx.x] = a.esc_ok[threadIdx.x];
+  s_vbad[threadIdx.x] = ((a.esc_ok[threadIdx.x >> 5] >> (threadIdx.x & 31)) & 1u) ^ 1u;
   for (int i = lane; i < kMarkWinWords / 4; i += 32)
     reinterpret_cast<uint4*>(S.bits)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
@@ -276,65 +277,88 @@ __global__ void __launch_bounds__(kMarkWarps * 32) escape_marks_kernel(const Mar
       const uint8_t* const val_w = a.values + o_lo;
       const uint32_t chunk32 = a.chunk;
       // Rounds of 32 consecutive ordinals (coalesced loads, the next 4
-      // rounds' in flight); each round's chunks from the previous round's
-      // (one compare when it crosses at most one chunk start).  (A variant
-      // staging each lane's contiguous slice in shared memory and walking it
-      // with a running chunk index issued fewer loads but measured 2x slower:
-      // its per-ordinal branches and the staging stores' load latency.)
+      // rounds' in flight).  The chunk of each ordinal comes from the
+      // warp-uniform starts of the current chunk and the next two (s0, s1,
+      // s2 in registers): one compare when a round crosses at most one chunk
+      // start, a per-lane search from the current chunk otherwise.  An
+      // ordinal is its chunk's first exactly when it equals its chunk's
+      // start, which is all the increasing-position check needs besides the
+      // predecessor's position.  (A variant staging each lane's contiguous
+      // slice in shared memory and walking it with a running chunk index
+      // issued fewer loads but measured 2x slower: its per-ordinal branches
+      // and the staging stores' load latency.)
       constexpr int U = 4;
-      uint32_t cur = 0;          // srel[cur] <= the round's first ordinal
+      const uint8_t* const vbad = s_vbad;
+      uint32_t cur = 0, s0 = 0, s1 = 0, s2 = 0;
+      auto refill = [&]() {
+        s0 = srel[cur];
+        s1 = cur + 1 < nk ? srel[cur + 1] : ~0u;
+        s2 = cur + 2 <= nk ? srel[cur + 2] : ~0u;
+      };
+      refill();
       uint32_t carry_pv = 0;     // position of the previous round's last ordinal
-      uint32_t carry_k = ~0u;    // and its chunk (none before the first round)
       uint32_t pvs[U], vs[U];
       auto load_batch = [&](uint32_t b0, uint32_t (&pp)[U], uint32_t (&vv)[U]) {
         const PosT* const pb = pos_w + b0 + lane;
         const uint8_t* const vb = val_w + b0 + lane;
-        const uint32_t left = no - b0 - lane;  // > 32u exactly when ordinal 32u + lane exists
+        if (b0 + 32 * U <= no) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const bool in = static_cast<int32_t>(left) > 32 * u;
-          pp[u] = in ? static_cast<uint32_t>(pb[32 * u]) : 0u;
-          vv[u] = in ? static_cast<uint32_t>(vb[32 * u]) : 0u;
+          for (int u = 0; u < U; ++u) {
+            pp[u] = static_cast<uint32_t>(pb[32 * u]);
+            vv[u] = static_cast<uint32_t>(vb[32 * u]);
+          }
+        } else {
+          const uint32_t left = no - b0 - lane;  // > 32u exactly when ordinal 32u + lane exists
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool in = static_cast<int32_t>(left) > 32 * u;
+            pp[u] = in ? static_cast<uint32_t>(pb[32 * u]) : 0u;
+            vv[u] = in ? static_cast<uint32_t>(vb[32 * u]) : 0u;
+          }
         }
       };
       // one round of 32 ordinals; the bitmap OR is unconditional (a lane
-      // without a hit ORs 0 into word 0), the chunk search branch is
-      // warp-uniform (__any_sync), so the only divergent branch left is the
-      // rare failed check
+      // without a hit ORs 0 into word 0), so the only divergent branch left
+      // is the rare failed check
       auto round = [&](uint32_t br, uint32_t pv, uint32_t v) {
-        const uint32_t orl = br + lane, last = min(br + 31, no - 1);
-        uint32_t k = cur;
-        if (__any_sync(0xffffffffu, cur + 2 <= nk && srel[cur + 2] <= last)) {
+        const uint32_t orl = br + lane;
+        const bool full = br + 32 <= no;           // warp-uniform
+        const uint32_t last = full ? br + 31 : no - 1;
+        uint32_t k, sk;
+        if (s2 <= last) {                          // warp-uniform: 2+ chunk starts in the round
           uint32_t hi = nk;
+          k = cur;
           while (hi - k > 1) {
             const uint32_t mid = (k + hi) >> 1;
             if (srel[mid] <= orl) k = mid; else hi = mid;
           }
+          sk = srel[k];
+          cur = __shfl_sync(0xffffffffu, k, 31);
+          refill();
         } else {
-          k += cur + 1 < nk && srel[cur + 1] <= orl ? 1u : 0u;
+          const bool up = orl >= s1;
+          k = cur + (up ? 1u : 0u);
+          sk = up ? s1 : s0;
+          if (last >= s1) {                        // warp-uniform: the round crosses one start
+            ++cur;
+            s0 = s1;
+            s1 = s2;
+            s2 = cur + 2 <= nk ? srel[cur + 2] : ~0u;
+          }
         }
-        // an ordinal is its chunk's first exactly when its predecessor is
-        // in another chunk (offsets are monotone)
-        uint32_t kprev = __shfl_up_sync(0xffffffffu, k, 1);
         uint32_t prev = __shfl_up_sync(0xffffffffu, pv, 1);
-        if (lane == 0) {
-          kprev = carry_k;
-          prev = carry_pv;
-        }
-        cur = __shfl_sync(0xffffffffu, k, 31);
-        carry_k = cur;
+        if (lane == 0) prev = carry_pv;
         carry_pv = __shfl_sync(0xffffffffu, pv, 31);
         const int32_t rel = kbase + static_cast<int32_t>(k * chunk32 + pv);
-        const bool live = orl < no;
-        // one set test covers the domain and the in-book check
-        const bool val_ok = (s_esc_ok[v >> 5] >> (v & 31)) & 1u;
+        const bool live = full || orl < no;
         const bool over = pv >= chunk32, beyond = rel >= past;
-        const bool not_inc = k == kprev && prev >= pv;
-        if (__builtin_expect(live && (!val_ok || over || beyond || not_inc), 0)) {
+        const bool not_inc = orl != sk && prev >= pv;
+        // one byte-table test covers the domain and the in-book check
+        if (__builtin_expect(live && (vbad[v] | over | beyond | not_inc), 0)) {
           // rare: the reference's checks in order (codec.py:446-536)
           const uint64_t o = o_lo + orl;
           if (v >= a.exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-          else if (!val_ok) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+          else if (vbad[v]) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
           if (over) record_first(&a.status->first_inv[SZ_DEC_POS_OVER_CHUNK], o);
           else if (beyond) record_first(&a.status->first_inv[SZ_DEC_POS_PAST_END], o);
           else if (not_inc) record_first(&a.status->first_inv[SZ_DEC_POS_NOT_INC], o);
@@ -370,7 +394,7 @@ __global__ void __launch_bounds__(kMarkWarps * 32) escape_marks_kernel(const Mar
         const uint32_t pv = static_cast<uint32_t>(load_pos<POSB>(a.positions, o));
         const uint32_t v = a.values[o];
         const uint64_t idx = (ka + lo) * chunk + pv;
-        const bool in_book = !((s_esc_ok[v >> 5] >> (v & 31)) & 1u);
+        const bool in_book = s_vbad[v];   // (after the domain check)
         if (v >= a.exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
         else if (in_book) record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
         if (pv >= chunk) {
@@ -400,11 +424,10 @@ __global__ void __launch_bounds__(kMarkWarps * 32) escape_marks_kernel(const Mar
       *sq = make_uint4(0, 0, 0, 0);
       const uint64_t wd = wd0 + 4ull * (lane + 32 * j);
       if (wd + 4 <= a.n_words) *reinterpret_cast<uint4*>(a.mark_bits + wd) = q;
-      uint32_t c = __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+      tsum += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+      if ((j + 1) % pieces_per_tile == 0) {  // one warp sum per decode tile
 #pragma unroll
-      for (int d = 16; d >= 1; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
-      tsum += c;
-      if ((j + 1) % pieces_per_tile == 0) {
+        for (int d = 16; d >= 1; d >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, d);
         const uint64_t tile = (wd0 + 128ull * (j + 1) - 1) / a.tile_words;
         if (lane == 0 && tile * a.tile_words < a.n_words) a.tile_marks[tile] = tsum;
         tsum = 0;
@@ -529,8 +552,9 @@ __device__ __forceinline__ uint32_t merge_group(uint32_t e4, uint32_t mg, uint32
                                                 uint32_t vals_base, uint32_t sel_base,
                                                 uint32_t keep4, uint32_t* nondummy) {
   const uint32_t sel = lds_u32(sel_base + 4 * mg);
-  const uint32_t a0 = vals_base + (r & ~3u);
-  const uint32_t v4 = __funnelshift_r(lds_u32(a0), lds_u32(a0 + 4), 8 * (r & 3));
+  const uint32_t ad = vals_base + r;    // (vals_base need not be word aligned)
+  const uint32_t a0 = ad & ~3u;
+  const uint32_t v4 = __funnelshift_r(lds_u32(a0), lds_u32(a0 + 4), 8 * (ad & 3));
   *nondummy = (e4 ^ keep4) & __byte_perm(0xFFFFFFFFu, 0u, sel);
   return __byte_perm(v4, e4, sel);
 }
@@ -575,10 +599,13 @@ struct DecSmem {
   alignas(128) uint8_t sm[STAGES][TILE * Fmt<FMT>::kSmBits / 8];
   uint32_t bitmap[STAGES][TILE / 32];
   uint32_t slot_first[STAGES][kDecSlots];  // compact index of a slot's first escape
-  // escape values by (ordinal - ofirst); 8 bytes of slack for the decode
-  // warps' 4-byte window reads (merge_group) at the end of the run
-  alignas(16) uint8_t vals[STAGES][kDecValCap<FMT> + 8];
+  // escape values by (ordinal - ofirst), from byte vshift (< 16: the K3e
+  // stager keeps the run's 16-byte quads at their global alignment); 8
+  // bytes of slack for the decode warps' 4-byte window reads (merge_group)
+  // at the end of the run
+  alignas(16) uint8_t vals[STAGES][kDecValCap<FMT> + 32];
   uint64_t ofirst[STAGES];                 // ordinal of the tile's first escape
+  uint32_t vshift[STAGES];
   uint64_t off[kDecHelpers][kDecOffStage + 1];
   uint64_t meta[STAGES];
   uint64_t full[STAGES];
@@ -771,6 +798,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
         if (c < kDecValCap<FMT>) S.vals[s][c] = static_cast<uint8_t>(v);
       };
       uint64_t o_first = 0;
+      uint32_t vshift = 0;
       if constexpr (ABS) {
         // abs32: per-ordinal checks spread evenly over tiles (the staging
         // below only visits ordinals whose positions land in some tile)
@@ -806,41 +834,6 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
         const uint64_t t_first = a.offsets[tile];
         const uint64_t t_end = max(a.offsets[tile + 1], t_first);
         o_first = t_first;
-        if constexpr (!SENT) {
-          // K3e checked every value already: a plain copy of the tile's run
-          // (4-byte loads of the words inside [t_first, t_end), bytes at the ends)
-          const uint64_t o_hi = min(min(t_end, m), t_first + kDecValCap<FMT>);
-          const uint64_t w_lo = (t_first + 3) >> 2, w_hi = o_hi >> 2;
-          if (w_lo < w_hi && !(reinterpret_cast<uintptr_t>(a.values) & 3)) {
-            const uint32_t* vw = reinterpret_cast<const uint32_t*>(a.values);
-            for (uint64_t i = w_lo + lane; i < w_hi; i += 32) {
-              const uint32_t q = vw[i];
-              const uint32_t c = static_cast<uint32_t>(4 * i - t_first);
-              S.vals[s][c] = static_cast<uint8_t>(q);
-              S.vals[s][c + 1] = static_cast<uint8_t>(q >> 8);
-              S.vals[s][c + 2] = static_cast<uint8_t>(q >> 16);
-              S.vals[s][c + 3] = static_cast<uint8_t>(q >> 24);
-            }
-            if (lane < 3 && t_first + lane < 4 * w_lo)
-              S.vals[s][lane] = a.values[t_first + lane];
-            if (lane >= 3 && lane < 6 && 4 * w_hi + (lane - 3) < o_hi)
-              S.vals[s][4 * w_hi + (lane - 3) - t_first] = a.values[4 * w_hi + (lane - 3)];
-          } else {
-            for (uint64_t o = t_first + lane; o < o_hi; o += 32) S.vals[s][o - t_first] = a.values[o];
-          }
-        } else {
-          // the tile's values first — staged (first kDecValCap) and checked
-          // (codec.py:446-457) for every ordinal its marks reach — while its
-          // code plane is still in flight
-          const uint64_t o_hi = min(t_end, m);
-          for (uint64_t o = t_first + lane; o < o_hi; o += 32) {
-            const uint32_t v = a.values[o];
-            if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
-            else if (!in_book(v))
-              record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
-            if (o - t_first < kDecValCap<FMT>) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
-          }
-        }
         // The tile's marks come as K3s's element bitmap, loaded here right at
         // the claim (no wait for the code plane's TMA): lane-contiguous words,
         // one warp scan for the slots' first compact indices.
@@ -879,6 +872,53 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
         }
 #pragma unroll
         for (int k = 0; k < WPL; ++k) S.bitmap[s][lane * WPL + k] = wv[k];
+        if constexpr (!SENT) {
+          // K3e checked every value already: a plain copy of the tile's run.
+          // Its 16-byte-aligned interior (<= kDecValCap / 16 quads) is loaded
+          // with every load in flight at once — one memory latency after
+          // t_first instead of one per 32 words — and the < 16-byte head and
+          // tail by single lanes.
+          const uint64_t o_hi = min(min(t_end, m), t_first + kDecValCap<FMT>);
+          const uintptr_t vb = reinterpret_cast<uintptr_t>(a.values);
+          const uint64_t q_lo = (vb + t_first + 15) >> 4, q_hi = (vb + o_hi) >> 4;
+          if (o_hi > t_first && q_lo < q_hi) {
+            constexpr int kQPL = (kDecValCap<FMT> / 16 + 31) / 32;
+            const uint4* qp = reinterpret_cast<const uint4*>(q_lo << 4);
+            const uint32_t nq = static_cast<uint32_t>(q_hi - q_lo);
+            uint4 qv[kQPL];
+#pragma unroll
+            for (int j = 0; j < kQPL; ++j)
+              if (lane + 32u * j < nq) qv[j] = __ldg(qp + lane + 32 * j);
+            const uint64_t head_end = (q_lo << 4) - vb, tail_beg = (q_hi << 4) - vb;
+            const uint64_t eo = lane < 16 ? t_first + lane : tail_beg + (lane - 16);
+            const bool edge = lane < 16 ? eo < head_end : eo < o_hi;
+            const uint8_t eb = edge ? a.values[eo] : 0;
+            // staged from byte vshift = the run's global address mod 16, so
+            // every interior quad is one aligned 16-byte store
+            vshift = static_cast<uint32_t>((vb + t_first) & 15);
+            uint8_t* const dv = S.vals[s] + vshift;
+            const uint32_t c0 = static_cast<uint32_t>(head_end - t_first);
+#pragma unroll
+            for (int j = 0; j < kQPL; ++j)
+              if (lane + 32u * j < nq)
+                *reinterpret_cast<uint4*>(dv + c0 + 16u * (lane + 32u * j)) = qv[j];
+            if (edge) dv[eo - t_first] = eb;
+          } else {
+            for (uint64_t o = t_first + lane; o < o_hi; o += 32) S.vals[s][o - t_first] = a.values[o];
+          }
+        } else {
+          // the tile's values first — staged (first kDecValCap) and checked
+          // (codec.py:446-457) for every ordinal its marks reach — while its
+          // code plane is still in flight
+          const uint64_t o_hi = min(t_end, m);
+          for (uint64_t o = t_first + lane; o < o_hi; o += 32) {
+            const uint32_t v = a.values[o];
+            if (v >= exp_bins) record_first(&a.status->first_inv[SZ_DEC_VALUE_DOMAIN], o);
+            else if (!in_book(v))
+              record_first(&a.status->first_inv[SZ_DEC_VALUE_IN_BOOK], o);
+            if (o - t_first < kDecValCap<FMT>) S.vals[s][o - t_first] = static_cast<uint8_t>(v);
+          }
+        }
       } else if constexpr (ABS) {
         // the tile's ordinal range from K3a (abs_bounds_kernel); clamped,
         // so a corrupt (unsorted) stream only ever costs bounded reads
@@ -1052,7 +1092,10 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
         }
         }
       }
-      if (lane == 0) S.ofirst[s] = o_first;
+      if (lane == 0) {
+        S.ofirst[s] = o_first;
+        S.vshift[s] = vshift;
+      }
       __syncwarp();
       mbar_arrive(&S.staged[s]);
     }
@@ -1072,6 +1115,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
     const uint32_t sbytes = (full_slots * SBYTES) & ~15u;
     mbar_wait(&S.staged[s], ph);
     const uint64_t ofirst = S.ofirst[s];
+    const uint32_t vshift = S.vshift[s];
 #pragma unroll
     for (int i = 0; i < kDecItems; ++i) {
       const uint32_t slot = i * kThreads + tid;
@@ -1147,7 +1191,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
           const uint32_t sf = S.slot_first[s][slot];
           const uint32_t first = bm ? sf : 0u;
           if (first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
-            const uint32_t vbase = smem_addr(S.vals[s]);
+            const uint32_t vbase = smem_addr(S.vals[s]) + vshift;
             uint32_t r = first, nd_any = 0;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
@@ -1169,7 +1213,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
           bm &= bm - 1;
           const uint32_t code = (pick<CWORDS>(cw, j >> 3) >> (4 * (j & 7))) & 0xF;
           if (!SENT && code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-          const uint32_t v = escape_value<kDecValCap<FMT>>(S.vals[s], S.slot_first[s][slot], bm0,
+          const uint32_t v = escape_value<kDecValCap<FMT>>(S.vals[s] + vshift, S.slot_first[s][slot], bm0,
                                                            j, ofirst, m, a.values);
           const int g = j >> 2, sh = 8 * (j & 3);
 #pragma unroll
@@ -1233,7 +1277,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
         const uint32_t sf = S.slot_first[s][slot];
         const uint32_t first = bm ? sf : 0u;
         if (first + __popc(bm) <= static_cast<uint32_t>(kDecValCap<FMT>)) {
-          const uint32_t vbase = smem_addr(S.vals[s]);
+          const uint32_t vbase = smem_addr(S.vals[s]) + vshift;
           uint32_t r = first, nd_any = 0;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
@@ -1264,7 +1308,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
           code = static_cast<uint32_t>(((hi << 32) | lo) >> (bit & 31)) & 7;
         }
         if (!SENT && code != 0) record_first(&a.status->first_inv[SZ_DEC_NONDUMMY], e0 + j);
-        const uint32_t v = escape_value<kDecValCap<FMT>>(S.vals[s], S.slot_first[s][slot], bm0,
+        const uint32_t v = escape_value<kDecValCap<FMT>>(S.vals[s] + vshift, S.slot_first[s][slot], bm0,
                                                          j, ofirst, m, a.values);
         const int g = j >> 2, sh = 8 * (j & 3);
 #pragma unroll
