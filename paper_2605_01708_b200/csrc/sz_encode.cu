@@ -1249,51 +1249,60 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// K6: raw exponent bytes -> dense LE bitstream of `width` bits per value
-// (_pack_values / _pack_bits, codec.py:241-266).  Reads M from device memory
-// so it chains after the encoder without a host round trip.
-// FP8 escape values -> 5 / 4-bit little-endian stream (formats.py:167-189).
-// A thread packs 8 values (one 8-byte load) into `width` bytes; a block's
-// 256 x width output bytes are contiguous and 4-byte aligned, so they go
-// through shared memory and leave as coalesced 32-bit stores.
+// K6: raw exponent bytes -> dense LE bitstream of W bits per value
+// (_pack_values / _pack_bits, codec.py:241-266; formats.py:167-189), FP8
+// escape values at W = 5 / 4.  Reads M from device memory so it chains
+// after the encoder without a host round trip.
+// One thread per 32 values: 32 W-bit values are exactly W 32-bit
+// words of the LE stream, so a thread loads its 32 bytes (two 16-byte loads,
+// both in flight), places every value at a compile-time bit offset, and
+// stores its W words straight to global memory (a warp's stores cover one
+// contiguous 128 x W-byte run).  Unaligned pointers and the ragged end take
+// byte loads / stores.
+template <int W>
 __global__ void __launch_bounds__(kThreads)
-    pack_values_kernel(const uint8_t* __restrict__ vals, const uint64_t* m_ptr,
-                       uint64_t capacity, int width, uint8_t* __restrict__ out) {
-  __shared__ __align__(16) uint8_t sbuf[kThreads * 8];
+    pack_values32_kernel(const uint8_t* __restrict__ vals, const uint64_t* m_ptr,
+                         uint64_t capacity, uint8_t* __restrict__ out) {
   const uint64_t m = min(*m_ptr, capacity);
-  const uint64_t groups = (m + 7) / 8;
-  const uint64_t nbytes_total = (m * width + 7) / 8;
-  const int tid = threadIdx.x;
-  const bool v8 = !(reinterpret_cast<uintptr_t>(vals) & 7);
+  const uint64_t units = (m + 31) / 32;
+  const uint64_t nbytes_total = (m * W + 7) / 8;
+  const bool v16 = !(reinterpret_cast<uintptr_t>(vals) & 15);
   const bool o4 = !(reinterpret_cast<uintptr_t>(out) & 3);
-  for (uint64_t blk = blockIdx.x; blk * kThreads < groups; blk += gridDim.x) {
-    const uint64_t gi = blk * kThreads + tid;
-    uint64_t acc = 0;
-    if (gi < groups) {
-      uint64_t x;
-      if (v8 && gi * 8 + 8 <= m) {
-        x = __ldg(reinterpret_cast<const unsigned long long*>(vals) + gi);
-      } else {
-        x = 0;
-        for (int j = 0; j < 8; ++j)
-          if (gi * 8 + j < m) x |= static_cast<uint64_t>(vals[gi * 8 + j]) << (8 * j);
-      }
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < units;
+       u += stride) {
+    uint32_t x[8];
+    const bool full = u * 32 + 32 <= m;
+    if (v16 && full) {
+      const uint4* src = reinterpret_cast<const uint4*>(vals) + 2 * u;
+      const uint4 a = __ldg(src), b = __ldg(src + 1);
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+      x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc |= ((x >> (8 * j)) & 0xFFu) << (j * width);
+      for (int k = 0; k < 8; ++k) x[k] = 0;
+      for (int j = 0; j < 32; ++j)
+        if (u * 32 + j < m) x[j >> 2] |= static_cast<uint32_t>(vals[u * 32 + j]) << (8 * (j & 3));
     }
-    for (int b = 0; b < width; ++b) sbuf[tid * width + b] = static_cast<uint8_t>(acc >> (8 * b));
-    __syncthreads();
-    const uint64_t ob0 = blk * kThreads * width;   // multiple of 4 (kThreads x width)
-    for (int w = tid; w < kThreads * width / 4; w += kThreads) {
-      const uint64_t ob = ob0 + 4ull * w;
-      if (o4 && ob + 4 <= nbytes_total) {
-        *reinterpret_cast<uint32_t*>(out + ob) = reinterpret_cast<const uint32_t*>(sbuf)[w];
-      } else {
-        for (int b = 0; b < 4; ++b)
-          if (ob + b < nbytes_total) out[ob + b] = sbuf[4 * w + b];
-      }
+    uint32_t w[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t v = (x[j >> 2] >> (8 * (j & 3))) & ((1u << W) - 1u);
+      const int bit = j * W, k = bit >> 5, off = bit & 31;
+      w[k] |= v << off;
+      if (off + W > 32) w[k + 1] |= v >> (32 - off);
     }
-    __syncthreads();
+    const uint64_t ob = u * 4 * W;
+    if (o4 && ob + 4 * W <= nbytes_total) {
+      uint32_t* d = reinterpret_cast<uint32_t*>(out + ob);
+#pragma unroll
+      for (int k = 0; k < W; ++k) d[k] = w[k];
+    } else {
+      for (int b = 0; b < 4 * W; ++b)
+        if (ob + b < nbytes_total) out[ob + b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
+    }
   }
 }
 
@@ -1604,13 +1613,16 @@ int encode_impl(const void* d_words, const uint64_t* seg_addrs, uint32_t seg_shi
   // (append mode: the caller packs the whole stream once, after the last piece)
   if (exp_bits != 8 && out->escape_capacity && !out->d_escape_base) {
     if (!out->d_values_packed) return SZ_ECONFIG;
-    // one block per 2048 values of the capacity (blocks past M exit at once),
-    // at most 16 per SM with a grid-stride loop beyond
-    const uint64_t want = (out->escape_capacity + 8 * kThreads - 1) / (8 * kThreads);
-    const unsigned pg = static_cast<unsigned>(want < 148 * 16 ? (want ? want : 1) : 148 * 16);
-    pack_values_kernel<<<pg, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
-                                               out->escape_capacity, exp_bits,
-                                               out->d_values_packed);
+    // one thread per 32 values of the capacity (threads past M exit at
+    // once), at most 8 blocks per SM with a grid-stride loop beyond
+    const uint64_t want = (out->escape_capacity + 32 * kThreads - 1) / (32 * kThreads);
+    const unsigned pg = static_cast<unsigned>(want < 148 * 8 ? (want ? want : 1) : 148 * 8);
+    if (exp_bits == 5)
+      pack_values32_kernel<5><<<pg, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
+                                                      out->escape_capacity, out->d_values_packed);
+    else
+      pack_values32_kernel<4><<<pg, kThreads, 0, s>>>(out->d_values, out->d_n_escapes,
+                                                      out->escape_capacity, out->d_values_packed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return sz_record_cuda(e);
   }
