@@ -158,3 +158,60 @@ def test_dense_corruption_verdicts_match_oracle(fmt_id, chunk, rate, cb, n, dec_
                 assert exc.value.chunk == want, name
         checked += want is not None
     assert checked >= 10
+
+
+@pytest.mark.parametrize("fmt_id", [1, 2])
+@pytest.mark.parametrize("voff,poff", [(0, 0), (1, 0), (0, 1), (3, 2), (9, 3), (15, 1)])
+def test_packed_values_unaligned_buffers(fmt_id, voff, poff):
+    """K6 (escape values -> 5 / 4-bit stream) with the raw-value and packed
+    outputs at arbitrary byte offsets (the C ABI takes any pointers): its
+    16-byte-load and word-store fast paths fall back to bytes and the
+    stream is still the reference's _pack_values (codec.py:241-266); the
+    cases' M are not multiples of 32, so the ragged last unit is covered."""
+    m = sz()
+    from paper_2605_01708_b200 import _native as N
+    from paper_2605_01708_b200.codec import (EncodeBuffers, _config_params, launch_encode,
+                                             packed_nbytes)
+    n = 3 * 16384 + 77 + 131 * voff + 29 * poff
+    words, book = dense_case(fmt_id, n, 0.0789, 4, 7 + voff + 16 * poff)
+    fmt, cfg = config(fmt_id, 4, 1024, book)
+    ref = O.encode(words, O.Params(fmt_id, 4, False, 1024, False), book)
+    mm = int(ref["m"])
+    assert mm % 32
+    w = fmt.exp_bits
+    bufs = EncodeBuffers(n, cfg, mm, torch.device("cuda"))
+    vals_big = torch.zeros(mm + 64, dtype=torch.uint8, device="cuda")
+    pack_big = torch.zeros(packed_nbytes(mm, w) + 64, dtype=torch.uint8, device="cuda")
+    bufs.values = vals_big[voff:voff + mm]
+    bufs.values_packed = pack_big[poff:poff + packed_nbytes(mm, w)]
+    launch_encode(torch.from_numpy(words).cuda(), _config_params(cfg, cfg.codebook), bufs)
+    torch.cuda.synchronize()
+    assert int(bufs.m.item()) == mm
+    assert np.array_equal(bufs.values.cpu().numpy(), ref["escape_values"])
+    got = bufs.values_packed.cpu().numpy()
+    assert got.tobytes() == O.pack_le(ref["escape_values"], w)
+    # nothing written outside the packed section
+    assert not pack_big[:poff].any() and not pack_big[poff + packed_nbytes(mm, w):].any()
+
+
+@pytest.mark.parametrize("off", [0, 1, 5, 8, 15])
+@pytest.mark.parametrize("fmt_id,cb", [(0, 3), (0, 4)])
+def test_k3e_values_at_any_alignment(fmt_id, cb, off, dec_path):
+    """The K3e stagers copy a tile's value run with 16-byte loads staged at
+    the run's own address mod 16 (vshift); a values section at any byte
+    offset (e.g. sliced out of a container in HBM) decodes bit-exactly on
+    both decoder paths."""
+    m = sz()
+    from paper_2605_01708_b200.codec import EncodedStreams
+    n = 5 * 8192 + 333
+    words, book = dense_case(fmt_id, n, 0.0689, cb, 31 + off)
+    fmt, cfg = config(fmt_id, cb, 1024, book)
+    stream = m.RawTensorStream(fmt, torch.from_numpy(words).cuda())
+    enc = m.encode(stream, cfg)
+    big = torch.zeros(enc.n_escapes + 32, dtype=torch.uint8, device="cuda")
+    big[off:off + enc.n_escapes] = enc.escape_values
+    moved = EncodedStreams(enc.n_elements, enc.n_escapes, enc.packed_codes, enc.sign_mantissa,
+                           enc.chunk_counts, enc.escape_positions,
+                           big[off:off + enc.n_escapes], enc.codebook, enc.values_packed)
+    dec = m.decode(moved, cfg, enc.codebook)
+    assert torch.equal(dec.words, stream.words)
