@@ -628,11 +628,20 @@ struct DecSmem {
 // PRMT — top-8 3-bit decode BF16 2067 -> 2095, E5M2 1196 -> 1297 GB/s.
 template <int CB, int PMODE>
 constexpr bool kT12 = CB == 3 && PMODE == kPosMarked;
+// E4M3 decodes like E5M2 (one byte per element, twice BF16's elements per
+// byte of traffic): 3 CTAs per SM on a 3-stage ring.
+#ifdef SZ_E4_2CTA
+constexpr bool kFp8ThreeCtas = false;
+#else
+constexpr bool kFp8ThreeCtas = true;
+#endif
+template <int FMT>
+constexpr bool kDec3Ctas = FMT == SZ_E5M2 || (FMT == SZ_E4M3 && kFp8ThreeCtas);
 template <int FMT, int CB, int PMODE>
 constexpr int kDecStages = PMODE == kPosMarked ? (FMT == SZ_BF16 && !kT12<CB, PMODE> ? 4 : 3)
-                                               : (FMT == SZ_E5M2 ? 3 : 5);
+                                               : (kDec3Ctas<FMT> ? 3 : 5);
 template <int FMT, int PMODE>
-constexpr int kDecCtasPerSm = PMODE == kPosMarked || FMT == SZ_E5M2 ? 3 : 2;
+constexpr int kDecCtasPerSm = PMODE == kPosMarked || kDec3Ctas<FMT> ? 3 : 2;
 
 template <int FMT, int CB, int PMODE>
 __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
