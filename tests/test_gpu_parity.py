@@ -197,6 +197,9 @@ def test_errors_and_empty():
 @pytest.mark.parametrize("fmt_id,n,rate,chunk", [
     (0, 1 << 22, 0.0016, 1024), (0, (1 << 22) + 777, 0.0123, 256), (0, 3_000_001, 0.05, 4096),
     (1, 1 << 22, 0.0016, 1024), (1, (1 << 22) + 5, 0.0123, 65536), (2, 1 << 21, 0.05, 1024),
+    # FP8 at realistic rates over several K2b groups (~52-62 records per
+    # 32K-element tile: the two-records-per-lane gather, its >64 tail loop)
+    (1, (1 << 24) + 12345, 0.0019, 1024), (2, (1 << 23) + 3, 0.0016, 4096),
 ])
 def test_large_streams_match_oracle(fmt_id, n, rate, chunk):
     m = sz()
