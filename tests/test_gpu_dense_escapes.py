@@ -98,9 +98,11 @@ def _mutations(sec, chunk, rng):
         p = pos.copy()
         p[o] = p[o - 1]                         # not strictly increasing (or chunk start)
         out.append((f"dup@{o}", dict(sec, escape_positions=p)))
-        p = pos.copy()
-        p[o] = chunk if pos.dtype == np.uint16 else 255
-        out.append((f"over@{o}", dict(sec, escape_positions=p)))
+        over = chunk if pos.dtype == np.uint16 else 255
+        if over <= np.iinfo(pos.dtype).max:     # (a u16 position cannot reach chunk 65536)
+            p = pos.copy()
+            p[o] = over
+            out.append((f"over@{o}", dict(sec, escape_positions=p)))
         v = vals.copy()
         v[o] = O.tables(sec["book"], sec["fmt"])[1][0]  # an in-book exponent
         out.append((f"inbook@{o}", dict(sec, escape_values=v,
@@ -121,6 +123,10 @@ def _mutations(sec, chunk, rng):
 @pytest.mark.parametrize("fmt_id,chunk,rate,cb,n", [
     (0, 1024, 0.0789, 4, 5 * 8192 + 333), (0, 256, 0.05, 3, 3 * 8192 + 7),
     (1, 1024, 0.0689, 3, 3 * 16384 + 77),
+    # chunks longer than the decode tile: each tile checks only its share
+    # of the chunk's ordinals (the split must still see every corruption)
+    (0, 65536, 0.0016, 4, 4 * 65536 + 100), (1, 65536, 0.0123, 4, 3 * 65536 + 77),
+    (0, 32768, 0.0123, 3, 2 * 32768 + 9), (1, 65536, 0.0016, 4, 2 * 65536),
 ])
 def test_dense_corruption_verdicts_match_oracle(fmt_id, chunk, rate, cb, n, dec_path):
     m = sz()
