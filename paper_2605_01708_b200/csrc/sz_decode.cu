@@ -626,8 +626,15 @@ struct DecSmem {
 // its ring drops to 3 stages so 3 CTAs still fit an SM): one lookup per 4
 // elements instead of two pair lookups, their address arithmetic and a
 // PRMT — top-8 3-bit decode BF16 2067 -> 2095, E5M2 1196 -> 1297 GB/s.
-template <int CB, int PMODE>
-constexpr bool kT12 = CB == 3 && PMODE == kPosMarked;
+// FP8 decoders on the position paths (3 CTAs x 3 stages) use it too.
+#ifdef SZ_NO_T12_FP8
+constexpr bool kT12Fp8 = false;
+#else
+constexpr bool kT12Fp8 = true;
+#endif
+template <int CB, int PMODE, int FMT = SZ_BF16>
+constexpr bool kT12 = CB == 3 && (PMODE == kPosMarked ||
+                                  (kT12Fp8 && FMT != SZ_BF16 && PMODE != 0));
 // E4M3 decodes like E5M2 (one byte per element, twice BF16's elements per
 // byte of traffic): 3 CTAs per SM on a 3-stage ring.
 #ifdef SZ_E4_2CTA
@@ -685,7 +692,7 @@ __global__ void __launch_bounds__(kDecThreads, kDecCtasPerSm<FMT, PMODE>)
     s_lut2[i] = p.dec_lut[c0] | (p.dec_lut[c1] << 8) | (bad << 16);
   }
   const uint32_t lut2_base = smem_addr(s_lut2);
-  constexpr bool T12 = kT12<CB, PMODE>;
+  constexpr bool T12 = kT12<CB, PMODE, FMT>;
   __shared__ __align__(16) uint32_t s_t12[T12 ? 4096 : 1];
   if constexpr (T12) {
     for (int i = tid; i < 4096; i += kDecThreads)
