@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--elements", type=int, default=None,
                     help="test only: elements per rank instead of the workload's "
                          "(recorded in config.elements_override)")
+    ap.add_argument("--no-chunk-sweep", action="store_true",
+                    help="skip config 2's chunk-size sweep (c2, one rank)")
     ap.add_argument("--no-handoff", action="store_true",
                     help="skip the N>=2 prefill->decode handoff leg (config 5)")
     return ap.parse_args()
@@ -326,6 +328,41 @@ def run_ours(args) -> None:
     # decode steps measured 52 / 105 / 123 ms with it, 51-57 ms without)
     clocks = sampler.stop()
 
+    # ---- config 2's chunk-size sweep (BASELINE configs[1]): the same words
+    # and book, one codec per chunk size, bitwise-verified, then 3 warm-up +
+    # 5 device-timed round trips each (outside the timed region above)
+    chunk_sweep = None
+    if wl["name"] == "c2" and world == 1 and not args.no_chunk_sweep:
+        chunk_sweep = []
+        for c in (256, 1024, 4096, 16384, 65536):
+            e_c = DeviceCodec(sz.CodecConfig(fmt, 4, chunk_size=c, codebook=book), book, n)
+            m_c = e_c.ensure_capacity(words)
+            e_c.decode()
+            e_c.check_status()
+            assert int(e_c.compare(words, e_c.out)[0].item()) == 0, f"chunk {c}: mismatch"
+            for _ in range(3):
+                e_c.encode(words)
+                e_c.decode()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(11)]
+            torch.cuda.synchronize()
+            for r in range(5):
+                evs[2 * r].record(stream)
+                e_c.encode(words)
+                evs[2 * r + 1].record(stream)
+                e_c.decode()
+            evs[10].record(stream)
+            torch.cuda.synchronize()
+            e_c.check_status()
+            ems = sum(evs[2 * r].elapsed_time(evs[2 * r + 1]) for r in range(5))
+            dms = sum(evs[2 * r + 1].elapsed_time(evs[2 * r + 2]) for r in range(5))
+            raw = n * fmt.word_nbytes
+            chunk_sweep.append({"chunk": c, "escapes": int(m_c),
+                                "encode_gbs": round(5 * raw / (ems / 1e3) / 1e9, 1),
+                                "decode_gbs": round(5 * raw / (dms / 1e3) / 1e9, 1),
+                                "compression_ratio": round(raw / e_c.payload_nbytes(m_c), 5)})
+            del e_c
+        torch.cuda.empty_cache()
+
     # ---- e2e through the public API with pinned host buffers
     host = torch.empty(n, dtype=fmt.torch_dtype, pin_memory=True)
     host.copy_(words)
@@ -438,6 +475,11 @@ def run_ours(args) -> None:
         "calibration_histogram_gbs": round(hist_gbs, 1),
         "clocks": clocks,
     }
+    if chunk_sweep is not None:
+        line["chunk_sweep"] = {"config": "BASELINE configs[1]: the same 2^31 words and book, "
+                                         "chunk 256..65536, 5 device-timed round trips each "
+                                         "after a bitwise check (outside the timed steps)",
+                               "points": chunk_sweep}
 
     if world >= 2 and world % 2 == 0 and not args.no_handoff and wl["fmt_id"] == 0:
         line["handoff"] = handoff_leg(rank, world, raw_baseline=backend == "nccl",
